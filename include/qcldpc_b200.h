@@ -1,0 +1,153 @@
+/*
+ * qcldpc_b200 -- C ABI of the B200-native LDPC / LDPCCC belief-propagation path.
+ *
+ * Every entry point replaces one numpy function of the reference package
+ * (/root/reference/pkg/src/qcldpc); the cited file:line is the interface it
+ * stands in for.  The Python host layer (paper_1204_0334_b200/_lib.py) binds
+ * these with ctypes; INTEGRATION.md shows the binding a maintainer of the
+ * reference would add.
+ *
+ * Conventions
+ *  - All array arguments are caller-owned DEVICE pointers (e.g. torch tensors),
+ *    except the host-side plan inputs of qc_plan_create_* (HOST pointers).
+ *  - gamma (lanes per batch, "Gamma" in the paper) must be a positive multiple
+ *    of 32; callers pad.  Lane g of a 32-lane word is bit (g & 31) of word g>>5.
+ *  - Message store: edge-major (E, gamma) fp32, edge ids row-major as in
+ *    codes.py:181-257.  Channel LLRs / posteriors: variable-major (N, gamma).
+ *    Hard-bit planes: (N, gamma/32) uint32.
+ *  - stream: a cudaStream_t passed as void*; 0 = legacy default stream.
+ *  - Return value: 0 ok; < 0 argument error (ValueError class); > 0 runtime /
+ *    CUDA error (RuntimeError class).  qc_last_error() gives the thread-local
+ *    message of the last failure.
+ *  - Plans are immutable after creation and safe to share across threads.
+ */
+#ifndef QCLDPC_B200_H
+#define QCLDPC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define QC_API __attribute__((visibility("default")))
+#else
+#define QC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qc_plan qc_plan;
+typedef struct cc_plan cc_plan;
+
+/* ---- errors / info ------------------------------------------------------ */
+QC_API const char* qc_last_error(void);
+QC_API int qc_abi_version(void);
+
+/* ---- code plans (replaces EdgeLayout/build_edge_layout, codes.py:181-257) */
+/* QC grid (J x L shifts, -1 = zero block), host pointer; replaces
+ * expand_qc + build_edge_layout (codes.py:159-178, 224-257). */
+QC_API int qc_plan_create_qc(const int64_t* shifts, int J, int L, int p, qc_plan** out);
+/* Arbitrary sparse H in the reference's row-major edge numbering:
+ * check_ptr (M+1), edge_var (E) -- EdgeLayout.check_ptr / .edge_var. */
+QC_API int qc_plan_create_csr(int n_vars, int n_checks, const int64_t* check_ptr,
+                       const int64_t* edge_var, qc_plan** out);
+QC_API void qc_plan_destroy(qc_plan* plan);
+/* dims[0..5] = N, M, E, dc_max, dv_max, check_regular (0 if irregular) */
+QC_API int qc_plan_dims(const qc_plan* plan, int64_t* dims);
+
+/* ---- block decoder kernels (bp.py) -------------------------------------- */
+/* MessageBatch.__init__ (bp.py:74-84): msgs[e] = mu[edge_var[e]]. */
+QC_API int qc_init(const qc_plan* plan, int gamma, const float* mu, float* msgs, void* stream);
+/* check_node_update (bp.py:134-162), in place; active = (gamma/32) lane-mask
+ * words or NULL (all lanes). */
+QC_API int qc_cnu(const qc_plan* plan, int gamma, float* msgs, const uint32_t* active,
+           void* stream);
+/* variable_node_update (bp.py:165-188): msgs <- beta, post (N,gamma) <- clip(total)
+ * (post may be NULL); hb (N,gamma/32) hard-bit planes of post (may be NULL). */
+QC_API int qc_vnu(const qc_plan* plan, int gamma, float* msgs, const float* mu, float* post,
+           uint32_t* hb, const uint32_t* active, void* stream);
+/* hard_decision_and_syndrome (bp.py:191-210) on hard-bit planes:
+ * bad[w] |= lanes of word w with an odd check (bad must be zeroed by caller). */
+QC_API int qc_syndrome(const qc_plan* plan, int gamma, const uint32_t* hb, uint32_t* bad,
+                void* stream);
+/* posterior -> hard-bit planes (bits = post < 0) */
+QC_API int qc_hard_bits(const qc_plan* plan, int gamma, const float* post, uint32_t* hb, void* stream);
+/* per-lane count of set hard bits (all-zero codeword => bit errors) */
+QC_API int qc_bit_errors(const qc_plan* plan, int gamma, const uint32_t* hb, int32_t* lane_bits,
+                  void* stream);
+
+/* decode_llr_batch (bp.py:213-265), whole loop on device.
+ * mu (N,gamma) clipped LLRs; msgs (E,gamma) scratch; post (N,gamma) out;
+ * hb (N,gamma/32) out; work: qc_decode_work_words(gamma) uint32 scratch;
+ * ok (gamma) u8 out; iters_run (gamma) i32 out; lane_bits (gamma) i32 out
+ * (may be NULL).  early_stop reproduces bp.py:242-256 (freeze on syndrome). */
+QC_API size_t qc_decode_work_words(int gamma);
+QC_API int qc_decode(const qc_plan* plan, int gamma, int iters, int early_stop, const float* mu,
+              float* msgs, float* post, uint32_t* hb, uint32_t* work, uint8_t* ok,
+              int32_t* iters_run, int32_t* lane_bits, void* stream);
+
+/* lane-major outputs (DecodeResult / DecodedFrame layout, bp.py:87-100,
+ * convolutional.py:166-177): post (n, gamma) fp32 -> post_out (gamma_out, n)
+ * fp64 and/or bits_out (gamma_out, n) u8 for the first gamma_out lanes
+ * (either output may be NULL). */
+QC_API int qc_lane_major(int n, int gamma, int gamma_out, const float* post, double* post_out,
+                  uint8_t* bits_out, void* stream);
+/* lane-major fp64 -> variable-major fp32 LLRs, lanes >= gamma_in padded with +50:
+ * sigma > 0: x are received values, mu = clip((2 x)/(sigma sigma), +-50) (channel_llrs, bp.py:54-56);
+ * sigma <= 0: x are LLRs, mu = clip(x, +-50) (decode_llr_batch, bp.py:231). */
+QC_API int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma,
+                                  float* mu_vm, void* stream);
+
+/* ---- channel (channel.py:61-105) ---------------------------------------- */
+/* y[g, k] = 1 + sigma * ndtri(u(philox word at position start+k of lane lane0+g)),
+ * mu = clip(2y/sigma^2, +-50) (bp.py:54-56).  Outputs (any may be NULL):
+ *   mu_vm  (n, gamma) fp32 variable-major LLRs,
+ *   y_lm   (gamma, n) fp64 lane-major received values,
+ *   g_lm   (gamma, n) fp64 lane-major standard normals (lane_normals). */
+QC_API int qc_channel(uint64_t seed_lo, uint64_t seed_hi, uint64_t lane0, uint64_t start, int n,
+               int gamma, double sigma, float* mu_vm, double* y_lm, double* g_lm,
+               void* stream);
+/* Same, first lane read from device memory (*lane0_dev) so a captured CUDA
+ * graph can be replayed for successive batches. */
+QC_API int qc_channel_dev(uint64_t seed_lo, uint64_t seed_hi, const uint64_t* lane0_dev, uint64_t start,
+                          int n, int gamma, double sigma, float* mu_vm, void* stream);
+/* *lane0_dev += k */
+QC_API int qc_lane_advance(uint64_t* lane0_dev, uint64_t k, void* stream);
+
+/* ---- campaign counters (harness.py:144-154) ----------------------------- */
+/* counts[b] = (frames, bit_errors, frame_errors) of lanes [b*gamma_ref, (b+1)*gamma_ref),
+ * counts (gamma/gamma_ref, 3) int64, accumulated (+=). */
+QC_API int qc_batch_counts(int gamma, int gamma_ref, const int32_t* lane_bits, int64_t* counts,
+                    void* stream);
+
+/* ---- LDPCCC stream decoder (convolutional.py:180-357) ------------------- */
+/* Unwrapped code plan from the QC grid (LdpcccCode, convolutional.py:67-151). */
+QC_API int cc_plan_create(const int64_t* shifts, int J, int L, int p, cc_plan** out);
+QC_API void cc_plan_destroy(cc_plan* plan);
+/* dims: lam, ms, c, cb, edge_count, sub_j, sub_l, p */
+QC_API int cc_plan_dims(const cc_plan* plan, int64_t* dims);
+/* One time slot of StreamDecoder._advance (convolutional.py:252-337):
+ * entry of frame t, I check-layer updates, I frame updates, emission.
+ *   msg   (I*E, gamma) fp32 message store,
+ *   ring  (I*(ms+1), c, gamma) fp32 channel-LLR ring,
+ *   mu_in (c, gamma) fp32 LLRs of frame t (NULL = zero-LLR virtual frame, flush),
+ *   post_out (c, gamma) fp32 posterior of the emitted frame t-I(ms+1)+1 (may be NULL),
+ *   lane_cnt (3, gamma) i32 (may be NULL): row 0 scratch, row 1 += bit errors,
+ *   row 2 += frame errors of every emitted frame (harness.py:228-232).
+ * t_dev: if non-NULL the slot index is *t_dev + t (device-resident slot
+ * counter, so a CUDA graph of K slots can be replayed; see cc_advance). */
+QC_API int cc_slot(const cc_plan* plan, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg,
+            float* ring, const float* mu_in, float* post_out, int32_t* lane_cnt, void* stream);
+/* *t_dev += k (ends a graph of k slots). */
+QC_API int cc_advance(int64_t* t_dev, int64_t k, void* stream);
+/* Channel for stream segments: frame t of lanes lane0.. at positions t*c
+ * (harness.py:226-227), LLRs straight into mu (c, gamma); t_dev as in cc_slot. */
+QC_API int cc_channel(const cc_plan* plan, uint64_t seed_lo, uint64_t seed_hi, uint64_t lane0,
+                      const uint64_t* lane0_dev, int64_t t, const int64_t* t_dev, int gamma,
+                      double sigma, float* mu, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

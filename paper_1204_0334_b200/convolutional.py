@@ -1,0 +1,177 @@
+"""LDPC convolutional codes unwrapped from QC-LDPC block codes, decoded on B200.
+
+Drop-in for /root/reference/pkg/src/qcldpc/convolutional.py.  `LdpcccCode`
+carries the same host attributes (lam, ms, c, cb, label_grid, lut_c, lut_v,
+lut_sub, sub_offset, edge_count, period, rate_bound; convolutional.py:67-151);
+`StreamDecoder` keeps its state on the GPU -- I processor groups of message
+packages and the I*(m_s+1)-frame channel ring (circular window in HBM) -- and
+advances one slot per `push_frame` with three sm_100a kernels (csrc/stream.cu).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+from . import _lib
+from .codes import ExponentMatrix
+from .plan import StreamPlan, pad32, require_cuda
+
+__all__ = ["LdpcccCode", "DecodedFrame", "unwrap_qc", "StreamDecoder"]
+
+
+class LdpcccCode:
+    """Unwrapped (convolutional) form of a QC-LDPC block code."""
+
+    def __init__(self, exp: ExponentMatrix):
+        J, L = exp.block_rows, exp.block_cols
+        lam = math.gcd(J, L)
+        if lam < 2:
+            raise ValueError(
+                f"gcd(J, L) = {lam}: the shift grid cannot be partitioned into a square "
+                "sub-block grid, so there is nothing to unwrap")
+        self.exp = exp
+        self.lam = lam
+        self.ms = lam - 1
+        self.p = exp.p
+        self.sub_j = J // lam
+        self.sub_l = L // lam
+        self.c = self.sub_l * exp.p
+        self.cb = self.sub_j * exp.p
+        self.label_grid = np.arange(lam * lam, dtype=np.int64).reshape(lam, lam)
+        k = np.arange(lam)
+        # layer phase kappa couples frames kappa-ms..kappa; frame phase phi couples layers phi..phi+ms
+        self.lut_c = self.label_grid[k[:, None], (k[:, None] + 1 + k[None, :]) % lam]
+        self.lut_v = self.label_grid[(k[:, None] + k[None, :]) % lam, k[:, None]]
+        sj, sl = self.sub_j, self.sub_l
+        self.lut_sub = [exp.shifts[(b // lam) * sj:(b // lam + 1) * sj, (b % lam) * sl:(b % lam + 1) * sl]
+                        for b in range(lam * lam)]
+        self.sub_edge_count = np.array([int((g >= 0).sum()) * self.p for g in self.lut_sub],
+                                       dtype=np.int64)
+        self.sub_offset = np.concatenate([[0], np.cumsum(self.sub_edge_count)[:-1]]).astype(np.int64)
+        self.edge_count = int(self.sub_edge_count.sum())
+        self._plan = None
+
+    @property
+    def period(self) -> int:
+        return self.lam
+
+    @property
+    def rate_bound(self) -> float:
+        return (self.c - self.cb) / self.c
+
+    def plan(self) -> StreamPlan:
+        if self._plan is None:
+            self._plan = StreamPlan(self.exp)
+            if (self._plan.E != self.edge_count or self._plan.c != self.c
+                    or self._plan.lam != self.lam):
+                raise RuntimeError("device LDPCCC plan does not match the host tables")
+        return self._plan
+
+
+def unwrap_qc(exp: ExponentMatrix) -> LdpcccCode:
+    """Unwrapped convolutional code of a QC grid; ValueError when gcd(J, L) < 2."""
+    return LdpcccCode(exp)
+
+
+@dataclasses.dataclass
+class DecodedFrame:
+    """Emitted frame: lane-major hard bits / posteriors; tail=True for flushed frames."""
+
+    frame_index: int
+    hard_bits: np.ndarray
+    posteriors: np.ndarray
+    tail: bool = False
+
+
+class StreamDecoder:
+    """Pipelined window decoder with I processors over gamma lanes (GPU-resident).
+
+    Frame t pushed at slot t is emitted at slot t + I*(m_s+1) - 1 after I
+    iterations; the first emission happens at slot I*(m_s+1) - 1.
+    """
+
+    def __init__(self, code: LdpcccCode, processors: int, gamma: int = 1):
+        if processors < 1:
+            raise ValueError("need at least one processor")
+        if gamma < 1:
+            raise ValueError("gamma must be positive")
+        torch = require_cuda()
+        self.code = code
+        self.processors = processors
+        self.gamma = gamma
+        self.period = code.ms + 1
+        self.window = processors * self.period
+        self.t = 0
+        self._flushed = False
+        self._gp = pad32(gamma)
+        self._plan = code.plan()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._msg = torch.zeros((processors * code.edge_count, self._gp), dtype=torch.float32, device=dev)
+        self._ring = torch.zeros((self.window, code.c, self._gp), dtype=torch.float32, device=dev)
+        self._mu = torch.empty((code.c, self._gp), dtype=torch.float32, device=dev)
+        self._post = torch.zeros((code.c, self._gp), dtype=torch.float32, device=dev)
+        self._y = torch.empty((gamma, code.c), dtype=torch.float64, device=dev)
+
+    @property
+    def channel_memory(self) -> np.ndarray:
+        """Channel LLR ring, (I*(m_s+1), c, gamma)."""
+        return self._ring[:, :, : self.gamma].double().cpu().numpy()
+
+    @property
+    def message_memory(self) -> np.ndarray:
+        """Edge message packages, (I, base edge count, gamma)."""
+        m = self._msg[:, : self.gamma].double().cpu().numpy()
+        return m.reshape(self.processors, self.code.edge_count, self.gamma)
+
+    def push_frame(self, y_frame: np.ndarray, sigma: float) -> DecodedFrame | None:
+        """Feed one received frame (gamma, c); return the emitted frame or None."""
+        if self._flushed:
+            raise RuntimeError("decoder already flushed; create a new one")
+        y = np.atleast_2d(np.asarray(y_frame, dtype=np.float64))
+        if y.shape != (self.gamma, self.code.c):
+            raise ValueError(f"expected frame shape {(self.gamma, self.code.c)}, got {y.shape}")
+        import torch
+        self._y.copy_(torch.from_numpy(np.ascontiguousarray(y)))
+        s = abs(float(sigma))
+        _lib.call("qc_llr_from_lane_major", self.code.c, self._gp, self.gamma, self._y.data_ptr(),
+                  s if s > 0.0 else 1e-300, self._mu.data_ptr(), _lib.stream_handle())
+        return self._advance(self._mu, tail=False)
+
+    def push_llr_device(self, mu_dev) -> DecodedFrame | None:
+        """B200 extension: push a frame of LLRs already on the device, (c, gamma_pad) fp32."""
+        if self._flushed:
+            raise RuntimeError("decoder already flushed; create a new one")
+        return self._advance(mu_dev, tail=False)
+
+    def flush(self) -> list:
+        """Push zero-LLR virtual frames until every real frame has left; frames flagged tail."""
+        if self._flushed:
+            raise RuntimeError("decoder already flushed")
+        out = []
+        for _ in range(self.window - 1):
+            fr = self._advance(None, tail=True)
+            if fr is not None:
+                out.append(fr)
+        self._flushed = True
+        return out
+
+    def _advance(self, mu_dev, tail: bool) -> DecodedFrame | None:
+        t = self.t
+        j = t - self.window + 1
+        _lib.call("cc_slot", self._plan.handle, self.processors, self._gp, t, None,
+                  self._msg.data_ptr(), self._ring.data_ptr(), _lib.ptr(mu_dev),
+                  self._post.data_ptr() if j >= 0 else None, None, _lib.stream_handle())
+        self.t = t + 1
+        if j < 0:
+            return None
+        import torch
+        c = self.code.c
+        post_d = torch.empty((self.gamma, c), dtype=torch.float64, device=self._post.device)
+        bits_d = torch.empty((self.gamma, c), dtype=torch.uint8, device=self._post.device)
+        _lib.call("qc_lane_major", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
+                  bits_d.data_ptr(), _lib.stream_handle())
+        return DecodedFrame(frame_index=j, hard_bits=bits_d.cpu().numpy(),
+                            posteriors=post_d.cpu().numpy(), tail=tail)

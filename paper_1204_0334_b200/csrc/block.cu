@@ -1,0 +1,687 @@
+// Batched flooding sum-product decoder for LDPC block codes on sm_100a.
+//
+// Replaces the numpy hot loop of /root/reference/pkg/src/qcldpc/bp.py:
+//   MessageBatch init (bp.py:74-84), check_node_update (bp.py:134-162),
+//   variable_node_update (bp.py:165-188), hard_decision_and_syndrome
+//   (bp.py:191-210) and decode_llr_batch (bp.py:213-265).
+//
+// Layout (paper's Gamma-codeword packages): the message
+// store is edge-major (E, gamma) fp32, so the gamma messages of one Tanner
+// edge are contiguous (gamma*4 bytes, 128-byte aligned for gamma % 32 == 0).
+// One thread owns VEC consecutive lanes of a package (float4 / float2 / float
+// loads), consecutive threads walk the lanes of the same package, so every
+// package read or write is a fully coalesced 128-bit access.
+//
+// Check pass: one thread = (check m, lane vector q); its d_c packages are
+// contiguous in the row-major edge order (codes.py:186-188), loaded up front
+// into registers (d_c independent 128-bit loads in flight per thread).
+// Variable pass: one thread = (variable n, lane vector q); its d_v package
+// addresses come from QC shift arithmetic (shift grid staged in shared
+// memory) or, for non-QC / irregular codes, from a padded var table.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "phi.cuh"
+#include "plan.h"
+
+using namespace qcb;
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// QC arithmetic (regular grid: every block live)
+// edge id of (block row j, circulant row r, block col l) = (j*p + r)*L + l
+// variable of that edge = l*p + (r + s_jl) mod p          (codes.py:159-178)
+// ----------------------------------------------------------------------------
+struct QcGrid {
+  int J, L, p;
+  int16_t s[QC_MAX_J * QC_MAX_L];
+};
+
+__device__ __forceinline__ void stage_grid(const QcGrid& g, int16_t* sh) {
+  for (int i = threadIdx.x; i < g.J * g.L; i += blockDim.x) sh[i] = g.s[i];
+  __syncthreads();
+}
+
+struct CnuArgs {
+  float* msgs;
+  const float* mu;            // FROM_MU: beta^0 gathered from mu (fused init)
+  const int32_t* check_ptr;   // irregular codes
+  const int32_t* edge_var;    // FROM_MU without QC
+  const uint32_t* active;     // lane mask words or null
+  const int32_t* done;        // early-stop "all frozen" flag or null
+  int M, gamma;
+};
+
+// Check-node update on the registers of one thread: x[k][i] = beta of edge k,
+// lane i  ->  alpha.  deg <= DC (pads excluded), lanes not in `lanes` untouched.
+template <int DC, int VEC>
+__device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned lanes) {
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    if (!((lanes >> i) & 1u)) continue;
+    unsigned par = 0;
+    float S = 0.0f, mx = -1.0f;
+    int kmx = 0;
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+      if (k < deg) {
+        float b = x[k][i];
+        unsigned sb = __float_as_uint(b) & 0x80000000u;
+        float f = phi(fabsf(b));
+        par ^= sb;
+        if (f > mx) { mx = f; kmx = k; }
+        S = __fadd_rn(S, f);
+        x[k][i] = __uint_as_float(__float_as_uint(f) | sb);   // signed phi
+      }
+    }
+    float S2 = 0.0f;   // exclusive sum of the dominant edge, summed directly
+#pragma unroll
+    for (int k = 0; k < DC; ++k)
+      if (k < deg && k != kmx) S2 = __fadd_rn(S2, fabsf(x[k][i]));
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+      if (k < deg) {
+        unsigned u = __float_as_uint(x[k][i]);
+        float f = __uint_as_float(u & 0x7fffffffu);
+        float mag = (k == kmx) ? S2 : __fsub_rn(S, f);
+        float a = fminf(phi(mag), ALPHA_CAP);
+        x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par) & 0x80000000u));
+      }
+    }
+  }
+}
+
+template <int DC, int VEC, bool REG, bool FROM_MU, bool QC>
+__global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid) {
+  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
+  if constexpr (QC && FROM_MU) stage_grid(grid, sh);
+  if (a.done && *a.done) return;
+  const int GV = a.gamma / VEC;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)a.M * GV) return;
+  int m = (int)(tid / GV), q = (int)(tid - (long long)m * GV);
+  int e0, deg;
+  if constexpr (REG) { e0 = m * DC; deg = DC; }
+  else { e0 = a.check_ptr[m]; deg = a.check_ptr[m + 1] - e0; }
+  unsigned lanes = lane_bits_of(a.active, q * VEC, VEC);
+  if (lanes == 0) return;   // frozen lanes keep their packages (bp.py:154-157)
+  float x[DC][VEC];
+  int jrow = 0, r = 0;
+  if constexpr (QC) { jrow = m / grid.p; r = m - jrow * grid.p; }
+#pragma unroll
+  for (int k = 0; k < DC; ++k) {
+    if (k < deg) {
+      if constexpr (FROM_MU) {
+        int v;
+        if constexpr (QC) {
+          int c = r + sh[jrow * grid.L + k];
+          c -= (c >= grid.p) ? grid.p : 0;
+          v = k * grid.p + c;
+        } else {
+          v = a.edge_var[e0 + k];
+        }
+        vload<VEC>(a.mu + (size_t)v * a.gamma + q * VEC, x[k]);
+      } else {
+        vload<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
+      }
+    }
+  }
+  if constexpr (FROM_MU) {
+    // frozen lanes inside the vector must see their stored packages
+    if (lanes != (1u << VEC) - 1u) {
+#pragma unroll
+      for (int k = 0; k < DC; ++k) {
+        if (k < deg) {
+          float old[VEC];
+          vload<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, old);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i)
+            if (!((lanes >> i) & 1u)) x[k][i] = old[i];
+        }
+      }
+    }
+  }
+  cnu_core<DC, VEC>(x, deg, lanes);
+#pragma unroll
+  for (int k = 0; k < DC; ++k)
+    if (k < deg) vstore<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
+}
+
+struct VnuArgs {
+  float* msgs;
+  const float* mu;
+  float* post;               // (N, gamma) or null
+  uint32_t* hb;              // (N, gamma/32) or null
+  const int32_t* var_pad;    // (N, DV) edge ids, -1 pad (non-QC)
+  const uint32_t* active;
+  const int32_t* done;
+  int N, gamma, dv;          // dv = table width
+  int write_beta;
+};
+
+template <int DV, int VEC, bool QC>
+__global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_constant__ QcGrid grid) {
+  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
+  if constexpr (QC) stage_grid(grid, sh);
+  if (a.done && *a.done) return;
+  const int GV = a.gamma / VEC;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = tid < (long long)a.N * GV;
+  int n = valid ? (int)(tid / GV) : 0;
+  int q = valid ? (int)(tid - (long long)n * GV) : 0;
+  unsigned lanes = valid ? lane_bits_of(a.active, q * VEC, VEC) : 0u;
+  int e[DV];
+  int deg = 0;
+  if constexpr (QC) {
+    int l = n / grid.p, c = n - l * grid.p;
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      int rr = c - sh[j * grid.L + l];
+      rr += (rr < 0) ? grid.p : 0;
+      e[j] = (j * grid.p + rr) * grid.L + l;
+    }
+    deg = DV;
+  } else {
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      e[j] = (j < a.dv && valid) ? a.var_pad[(size_t)n * a.dv + j] : -1;
+      deg += (e[j] >= 0);
+    }
+  }
+  float tot[VEC], am[DV][VEC];
+  unsigned bits = 0;
+  if (valid && lanes) {
+    vload<VEC>(a.mu + (size_t)n * a.gamma + q * VEC, tot);
+#pragma unroll
+    for (int j = 0; j < DV; ++j)
+      if (j < deg) vload<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, am[j]);
+    // running total in increasing edge order (bp.py:179-181)
+#pragma unroll
+    for (int j = 0; j < DV; ++j)
+      if (j < deg) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], am[j][i]);
+      }
+    if (a.write_beta) {
+      const bool all = lanes == (1u << VEC) - 1u;
+#pragma unroll
+      for (int j = 0; j < DV; ++j)
+        if (j < deg) {
+          float b[VEC];
+#pragma unroll
+          for (int i = 0; i < VEC; ++i)
+            b[i] = ((lanes >> i) & 1u) ? clampL(__fsub_rn(tot[i], am[j][i])) : am[j][i];
+          (void)all;
+          vstore<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, b);
+        }
+    }
+    float pst[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      pst[i] = clampL(tot[i]);
+      bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
+    }
+    if (a.post) {
+      if (lanes == (1u << VEC) - 1u) {
+        vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
+      } else {
+        for (int i = 0; i < VEC; ++i)
+          if ((lanes >> i) & 1u) a.post[(size_t)n * a.gamma + q * VEC + i] = pst[i];
+      }
+    }
+  }
+  if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, valid);
+}
+
+__global__ void init_kernel(const float* mu, float* msgs, const int32_t* edge_var, int E, int gamma) {
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int GV = gamma / 4;
+  if (tid >= (long long)E * GV) return;
+  int e = (int)(tid / GV), q = (int)(tid - (long long)e * GV);
+  float v[4];
+  vload<4>(mu + (size_t)edge_var[e] * gamma + q * 4, v);
+  vstore<4>(msgs + (size_t)e * gamma + q * 4, v);
+}
+
+template <int DC>
+__global__ void syndrome_kernel(const uint32_t* hb, uint32_t* bad, const int32_t* check_ptr,
+                                const int32_t* edge_var, int M, int W, const int32_t* done) {
+  if (done && *done) return;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)M * W) return;
+  int m = (int)(tid / W), w = (int)(tid - (long long)m * W);
+  int e0 = check_ptr[m], deg = check_ptr[m + 1] - e0;
+  uint32_t par = 0;
+  for (int k = 0; k < deg; ++k) par ^= hb[(size_t)edge_var[e0 + k] * W + w];
+  if (par) atomicOr(bad + w, par);
+}
+
+__global__ void hard_bits_kernel(const float* post, uint32_t* hb, int N, int gamma) {
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int GV = gamma / 4;
+  bool valid = tid < (long long)N * GV;
+  int n = valid ? (int)(tid / GV) : 0, q = valid ? (int)(tid - (long long)n * GV) : 0;
+  unsigned bits = 0;
+  if (valid) {
+    float v[4];
+    vload<4>(post + (size_t)n * gamma + q * 4, v);
+    for (int i = 0; i < 4; ++i) bits |= (v[i] < 0.0f ? 1u : 0u) << i;
+  }
+  store_bit_word<4>(hb + (size_t)n * (gamma >> 5), q, bits, valid);
+}
+
+// per-lane popcount over variables: block (word w, variable chunk)
+__global__ void bit_errors_kernel(const uint32_t* hb, int32_t* lane_bits, int N, int W) {
+  __shared__ int cnt[32];
+  int w = blockIdx.y;
+  if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int c[32];
+#pragma unroll
+  for (int b = 0; b < 32; ++b) c[b] = 0;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    uint32_t x = hb[(size_t)n * W + w];
+    if (x) {
+#pragma unroll
+      for (int b = 0; b < 32; ++b) c[b] += (x >> b) & 1u;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 32; ++b) {
+    int v = c[b];
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cnt[b], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && cnt[threadIdx.x]) atomicAdd(lane_bits + w * 32 + threadIdx.x, cnt[threadIdx.x]);
+}
+
+// early-stop bookkeeping after iteration `it` (bp.py:242-256): lanes that are
+// active and syndrome-clean freeze; bad words are consumed and cleared.
+__global__ void es_update_kernel(uint32_t* active, uint32_t* bad, int32_t* iters_run, int32_t* done,
+                                 int W, int it) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  if (*done) return;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    uint32_t act = active[w];
+    uint32_t stop = act & ~bad[w];
+    for (int b = 0; b < 32; ++b)
+      if ((stop >> b) & 1u) iters_run[w * 32 + b] = it;
+    act &= ~stop;
+    active[w] = act;
+    bad[w] = 0;
+    if (act) any = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && !any) *done = 1;
+}
+
+__global__ void es_start_kernel(uint32_t* active, uint32_t* bad, int32_t* iters_run, int32_t* done,
+                                int W, int iters) {
+  for (int w = threadIdx.x + blockIdx.x * blockDim.x; w < W; w += blockDim.x * gridDim.x) {
+    active[w] = 0xffffffffu;
+    bad[w] = 0;
+    for (int b = 0; b < 32; ++b) iters_run[w * 32 + b] = iters;
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *done = 0;
+}
+
+// ok[g] = lane passed the syndrome.  Early stop: ok = frozen (= !active);
+// plain decode: ok = !bad.
+__global__ void finalize_ok_kernel(const uint32_t* bad, const uint32_t* active, uint8_t* ok, int gamma) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= gamma) return;
+  uint32_t b = active ? active[g >> 5] : bad[g >> 5];
+  ok[g] = ((b >> (g & 31)) & 1u) ? 0 : 1;
+}
+
+__global__ void fill_i32(int32_t* p, int n, int v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// (N, gamma) fp32 -> (gamma_out, N) fp64 / u8 through a 32x32 smem tile
+__global__ void lane_major_kernel(const float* post, double* post_out, uint8_t* bits_out, int N,
+                                  int gamma, int gamma_out) {
+  __shared__ float tile[32][33];
+  int n0 = blockIdx.x * 32, g0 = blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int n = n0 + dy, g = g0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (n < N) ? post[(size_t)n * gamma + g] : 0.0f;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int g = g0 + dy, n = n0 + threadIdx.x;
+    if (g < gamma_out && n < N) {
+      float v = tile[threadIdx.x][dy];
+      if (post_out) post_out[(size_t)g * N + n] = (double)v;
+      if (bits_out) bits_out[(size_t)g * N + n] = v < 0.0f ? 1 : 0;
+    }
+  }
+}
+
+// lane-major fp64 (received values or LLRs) -> variable-major fp32 LLRs, in
+// the reference's operation order: clip((2*y)/(sigma*sigma), +-50) (bp.py:54-56)
+// when sigma > 0, clip(x, +-50) otherwise (bp.py:231); padded lanes get +50.
+__global__ void llr_from_lane_major_kernel(const double* x, float* mu, int N, int gamma,
+                                           int gamma_in, double sigma) {
+  __shared__ float tile[32][33];
+  int n0 = blockIdx.x * 32, g0 = blockIdx.y * 32;
+  const double s2 = __dmul_rn(sigma, sigma);
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int g = g0 + dy, n = n0 + threadIdx.x;
+    float v = 50.0f;
+    if (g < gamma_in && n < N) {
+      double t = x[(size_t)g * N + n];
+      if (sigma > 0.0) t = __ddiv_rn(__dmul_rn(2.0, t), s2);
+      t = t < -50.0 ? -50.0 : (t > 50.0 ? 50.0 : t);
+      v = __double2float_rn(t);
+    }
+    tile[dy][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int n = n0 + dy, g = g0 + threadIdx.x;
+    if (n < N) mu[(size_t)n * gamma + g] = tile[threadIdx.x][dy];
+  }
+}
+
+__global__ void batch_counts_kernel(const int32_t* lane_bits, int64_t* counts, int nb, int gref) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  long long be = 0, fe = 0;
+  for (int g = 0; g < gref; ++g) {
+    int v = lane_bits[b * gref + g];
+    be += v;
+    fe += v > 0;
+  }
+  counts[b * 3 + 0] += gref;
+  counts[b * 3 + 1] += be;
+  counts[b * 3 + 2] += fe;
+}
+
+// ----------------------------------------------------------------------------
+// dispatch
+// ----------------------------------------------------------------------------
+int bucket_dc(int d) {
+  static const int B[] = {2, 4, 6, 8, 12, 16, 24, 32};
+  for (int b : B)
+    if (d <= b) return b;
+  return -1;
+}
+int bucket_dv(int d) {
+  static const int B[] = {2, 3, 4, 6, 8, 12, 16};
+  for (int b : B)
+    if (d <= b) return b;
+  return -1;
+}
+
+int pick_vec(int gamma, int dc) {
+  if (dc > 24) return gamma % 64 == 0 ? 2 : 1;
+  if (gamma >= 128) return 4;
+  if (gamma >= 64) return 2;
+  return 1;
+}
+
+QcGrid make_grid(const qc_plan* p) {
+  QcGrid g;
+  std::memset(&g, 0, sizeof(g));
+  if (p->qc_regular) {
+    g.J = p->J; g.L = p->L; g.p = p->p;
+    for (int i = 0; i < p->J * p->L; ++i) g.s[i] = (int16_t)p->shifts[i];
+  }
+  return g;
+}
+
+template <int DC, int VEC>
+void launch_cnu_dv(const qc_plan* p, const CnuArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
+  long long threads = (long long)p->M * (a.gamma / VEC);
+  unsigned nb = blocks_for(threads);
+  const bool reg = p->check_regular == DC;
+  const bool qc = p->qc_regular;
+  if (from_mu) {
+    if (qc && reg) cnu_kernel<DC, VEC, true, true, true><<<nb, THREADS, 0, s>>>(a, g);
+    else if (reg) cnu_kernel<DC, VEC, true, true, false><<<nb, THREADS, 0, s>>>(a, g);
+    else cnu_kernel<DC, VEC, false, true, false><<<nb, THREADS, 0, s>>>(a, g);
+  } else {
+    if (reg) cnu_kernel<DC, VEC, true, false, false><<<nb, THREADS, 0, s>>>(a, g);
+    else cnu_kernel<DC, VEC, false, false, false><<<nb, THREADS, 0, s>>>(a, g);
+  }
+}
+
+template <int DC>
+void launch_cnu_vec(const qc_plan* p, const CnuArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
+  switch (pick_vec(a.gamma, DC)) {
+    case 4: launch_cnu_dv<DC, 4>(p, a, from_mu, g, s); break;
+    case 2: launch_cnu_dv<DC, 2>(p, a, from_mu, g, s); break;
+    default: launch_cnu_dv<DC, 1>(p, a, from_mu, g, s); break;
+  }
+}
+
+int launch_cnu(const qc_plan* p, CnuArgs a, bool from_mu, cudaStream_t s) {
+  if (p->E == 0 || p->M == 0) return 0;
+  QcGrid g = make_grid(p);
+  switch (bucket_dc(p->dc_max)) {
+    case 2: launch_cnu_vec<2>(p, a, from_mu, g, s); break;
+    case 4: launch_cnu_vec<4>(p, a, from_mu, g, s); break;
+    case 6: launch_cnu_vec<6>(p, a, from_mu, g, s); break;
+    case 8: launch_cnu_vec<8>(p, a, from_mu, g, s); break;
+    case 12: launch_cnu_vec<12>(p, a, from_mu, g, s); break;
+    case 16: launch_cnu_vec<16>(p, a, from_mu, g, s); break;
+    case 24: launch_cnu_vec<24>(p, a, from_mu, g, s); break;
+    case 32: launch_cnu_vec<32>(p, a, from_mu, g, s); break;
+    default: return fail_arg("check degree > 32 is not supported");
+  }
+  return check_launch("cnu");
+}
+
+template <int DV, int VEC>
+void launch_vnu_v(const qc_plan* p, const VnuArgs& a, const QcGrid& g, cudaStream_t s) {
+  long long threads = (long long)p->N * (a.gamma / VEC);
+  unsigned nb = blocks_for(threads);
+  if (p->qc_regular && p->J == DV) vnu_kernel<DV, VEC, true><<<nb, THREADS, 0, s>>>(a, g);
+  else vnu_kernel<DV, VEC, false><<<nb, THREADS, 0, s>>>(a, g);
+}
+
+template <int DV>
+void launch_vnu_vec(const qc_plan* p, const VnuArgs& a, const QcGrid& g, cudaStream_t s) {
+  int vec = a.gamma >= 128 ? 4 : (a.gamma >= 64 ? 2 : 1);
+  switch (vec) {
+    case 4: launch_vnu_v<DV, 4>(p, a, g, s); break;
+    case 2: launch_vnu_v<DV, 2>(p, a, g, s); break;
+    default: launch_vnu_v<DV, 1>(p, a, g, s); break;
+  }
+}
+
+int launch_vnu(const qc_plan* p, VnuArgs a, cudaStream_t s) {
+  QcGrid g = make_grid(p);
+  a.var_pad = p->d_var_pad;
+  a.dv = p->dv_max;
+  a.N = p->N;
+  if (p->N == 0) return 0;
+  switch (bucket_dv(std::max(p->dv_max, 1))) {
+    case 2: launch_vnu_vec<2>(p, a, g, s); break;
+    case 3: launch_vnu_vec<3>(p, a, g, s); break;
+    case 4: launch_vnu_vec<4>(p, a, g, s); break;
+    case 6: launch_vnu_vec<6>(p, a, g, s); break;
+    case 8: launch_vnu_vec<8>(p, a, g, s); break;
+    case 12: launch_vnu_vec<12>(p, a, g, s); break;
+    case 16: launch_vnu_vec<16>(p, a, g, s); break;
+    default: return fail_arg("variable degree > 16 is not supported");
+  }
+  return check_launch("vnu");
+}
+
+int check_gamma(int gamma) {
+  if (gamma <= 0 || gamma % 32) return fail_arg("gamma must be a positive multiple of 32, got " + std::to_string(gamma));
+  return 0;
+}
+
+int launch_syndrome(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, const int32_t* done,
+                    cudaStream_t s) {
+  int W = gamma / 32;
+  if (p->M == 0) return 0;
+  long long threads = (long long)p->M * W;
+  syndrome_kernel<0><<<blocks_for(threads), THREADS, 0, s>>>(hb, bad, p->d_check_ptr, p->d_edge_var, p->M, W, done);
+  return check_launch("syndrome");
+}
+
+int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s) {
+  int W = gamma / 32;
+  cudaMemsetAsync(lane_bits, 0, sizeof(int32_t) * gamma, s);
+  int chunks = std::max(1, std::min(64, (p->N + 255) / 256));
+  dim3 grid(chunks, W);
+  bit_errors_kernel<<<grid, 256, 0, s>>>(hb, lane_bits, p->N, W);
+  return check_launch("bit_errors");
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int qc_init(const qc_plan* p, int gamma, const float* mu, float* msgs, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !mu || !msgs) return fail_arg("null argument");
+  if (p->E == 0) return 0;
+  long long threads = (long long)p->E * (gamma / 4);
+  init_kernel<<<blocks_for(threads), THREADS, 0, as_stream(stream)>>>(mu, msgs, p->d_edge_var, p->E, gamma);
+  return check_launch("init");
+}
+
+int qc_cnu(const qc_plan* p, int gamma, float* msgs, const uint32_t* active, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !msgs) return fail_arg("null argument");
+  CnuArgs a{msgs, nullptr, p->d_check_ptr, p->d_edge_var, active, nullptr, p->M, gamma};
+  return launch_cnu(p, a, false, as_stream(stream));
+}
+
+int qc_vnu(const qc_plan* p, int gamma, float* msgs, const float* mu, float* post, uint32_t* hb,
+           const uint32_t* active, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !msgs || !mu) return fail_arg("null argument");
+  VnuArgs a{};
+  a.msgs = msgs; a.mu = mu; a.post = post; a.hb = hb; a.active = active; a.done = nullptr;
+  a.gamma = gamma; a.write_beta = 1;
+  return launch_vnu(p, a, as_stream(stream));
+}
+
+int qc_syndrome(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !hb || !bad) return fail_arg("null argument");
+  return launch_syndrome(p, gamma, hb, bad, nullptr, as_stream(stream));
+}
+
+int qc_hard_bits(const qc_plan* p, int gamma, const float* post, uint32_t* hb, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !post || !hb) return fail_arg("null argument");
+  long long threads = (long long)p->N * (gamma / 4);
+  hard_bits_kernel<<<blocks_for(threads), THREADS, 0, as_stream(stream)>>>(post, hb, p->N, gamma);
+  return check_launch("hard_bits");
+}
+
+int qc_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !hb || !lane_bits) return fail_arg("null argument");
+  return launch_bit_errors(p, gamma, hb, lane_bits, as_stream(stream));
+}
+
+size_t qc_decode_work_words(int gamma) {
+  // bad (W) | active (W) | done (1) | pad
+  size_t W = (size_t)(gamma > 0 ? gamma : 0) / 32;
+  return 2 * W + 4;
+}
+
+int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const float* mu, float* msgs,
+              float* post, uint32_t* hb, uint32_t* work, uint8_t* ok, int32_t* iters_run,
+              int32_t* lane_bits, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (iters < 1) return fail_arg("need at least one iteration");
+  if (!p || !mu || !msgs || !post || !hb || !work || !ok || !iters_run) return fail_arg("null argument");
+  cudaStream_t s = as_stream(stream);
+  const int W = gamma / 32;
+  uint32_t* bad = work;
+  uint32_t* active = work + W;
+  int32_t* done = reinterpret_cast<int32_t*>(work + 2 * W);
+  int rc = 0;
+  if (!early_stop) {
+    cudaMemsetAsync(bad, 0, sizeof(uint32_t) * W, s);
+    fill_i32<<<blocks_for(gamma), THREADS, 0, s>>>(iters_run, gamma, iters);
+    for (int it = 1; it <= iters; ++it) {
+      CnuArgs c{msgs, mu, p->d_check_ptr, p->d_edge_var, nullptr, nullptr, p->M, gamma};
+      if ((rc = launch_cnu(p, c, it == 1, s))) return rc;   // iteration 1: init fused (beta^0 = mu)
+      VnuArgs v{};
+      v.msgs = msgs; v.mu = mu; v.gamma = gamma;
+      v.write_beta = it < iters;      // the last beta is never read
+      v.post = it == iters ? post : nullptr;
+      v.hb = it == iters ? hb : nullptr;
+      if ((rc = launch_vnu(p, v, s))) return rc;
+    }
+    if ((rc = launch_syndrome(p, gamma, hb, bad, nullptr, s))) return rc;
+    finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, nullptr, ok, gamma);
+  } else {
+    es_start_kernel<<<1, 256, 0, s>>>(active, bad, iters_run, done, W, iters);
+    for (int it = 1; it <= iters; ++it) {
+      CnuArgs c{msgs, mu, p->d_check_ptr, p->d_edge_var, active, done, p->M, gamma};
+      if (it == 1) {
+        // materialise beta^0 so lanes that freeze keep a defined package
+        long long threads = (long long)p->E * (gamma / 4);
+        if (p->E) init_kernel<<<blocks_for(threads), THREADS, 0, s>>>(mu, msgs, p->d_edge_var, p->E, gamma);
+      }
+      if ((rc = launch_cnu(p, c, false, s))) return rc;
+      VnuArgs v{};
+      v.msgs = msgs; v.mu = mu; v.gamma = gamma; v.write_beta = 1;
+      v.post = post; v.hb = hb; v.active = active; v.done = done;
+      if ((rc = launch_vnu(p, v, s))) return rc;
+      if ((rc = launch_syndrome(p, gamma, hb, bad, done, s))) return rc;
+      es_update_kernel<<<1, 256, 0, s>>>(active, bad, iters_run, done, W, it);
+    }
+    finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, active, ok, gamma);
+    // hb must reflect the recorded posteriors of every lane (frozen lanes too)
+    long long threads = (long long)p->N * (gamma / 4);
+    hard_bits_kernel<<<blocks_for(threads), THREADS, 0, s>>>(post, hb, p->N, gamma);
+  }
+  if (lane_bits && (rc = launch_bit_errors(p, gamma, hb, lane_bits, s))) return rc;
+  return check_launch("decode");
+}
+
+int qc_lane_major(int n, int gamma, int gamma_out, const float* post, double* post_out, uint8_t* bits_out,
+                  void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (n < 0 || !post || gamma_out < 0 || gamma_out > gamma) return fail_arg("bad lane_major arguments");
+  if (n == 0 || gamma_out == 0) return 0;
+  dim3 grid((n + 31) / 32, (gamma_out + 31) / 32), block(32, 8);
+  lane_major_kernel<<<grid, block, 0, as_stream(stream)>>>(post, post_out, bits_out, n, gamma, gamma_out);
+  return check_launch("lane_major");
+}
+
+int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma, float* mu_vm,
+                           void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (n < 0 || gamma_in < 0 || gamma_in > gamma || (!x && gamma_in) || !mu_vm) return fail_arg("bad llr arguments");
+  if (n == 0) return 0;
+  dim3 grid((n + 31) / 32, gamma / 32), block(32, 8);
+  llr_from_lane_major_kernel<<<grid, block, 0, as_stream(stream)>>>(x, mu_vm, n, gamma, gamma_in, sigma);
+  return check_launch("llr_from_lane_major");
+}
+
+int qc_batch_counts(int gamma, int gamma_ref, const int32_t* lane_bits, int64_t* counts, void* stream) {
+  if (gamma_ref <= 0 || gamma <= 0 || gamma % gamma_ref) return fail_arg("gamma must be a multiple of gamma_ref");
+  int nb = gamma / gamma_ref;
+  batch_counts_kernel<<<blocks_for(nb), THREADS, 0, as_stream(stream)>>>(lane_bits, counts, nb, gamma_ref);
+  return check_launch("batch_counts");
+}
+
+}  // extern "C"

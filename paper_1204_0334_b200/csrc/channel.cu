@@ -1,0 +1,120 @@
+// On-device AWGN/BPSK channel + LLRs (replaces channel.py:61-105 and bp.py:54-56).
+//
+// Sample position q of lane l is 64-bit word q mod 4 of Philox4x64-10 with
+// key = seed (128-bit, two words) and counter = [q//4 + 1, l, 0, 0] -- numpy's
+// Philox pre-increments its 256-bit counter before producing a block, and the
+// reference seeds it at (l << 64) + start//4 (channel.py:70-74).  The word
+// maps to u = ((w >> 11) + 0.5) 2^-53 and g = ndtri(u) (Cephes inverse normal
+// CDF, the algorithm behind scipy.special.ndtri), all in fp64; then
+// y = 1 + sigma g and mu = clip(2 y / sigma^2, +-50) in the reference's
+// operation order, rounded once to fp32 for the message store.
+//
+// Thread mapping: consecutive threads = consecutive lanes of one Philox block
+// (4 consecutive positions), so the variable-major mu store (n, gamma) is a
+// coalesced 128-byte row per position.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "philox.cuh"
+
+using namespace qcb;
+
+namespace {
+
+struct ChanArgs {
+  uint64_t k0, k1, lane0, start;
+  const uint64_t* lane0_dev;   // optional: lane0 = *lane0_dev
+  const int64_t* t_dev;     // optional: start += (*t_dev + t_add) * t_mul
+  long long t_add, t_mul;
+  int n, gamma;
+  double sigma;
+  float* mu_vm;
+  double* y_lm;
+  double* g_lm;
+};
+
+__global__ void __launch_bounds__(THREADS) channel_kernel(ChanArgs a) {
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.t_dev) a.start += (uint64_t)((*a.t_dev + a.t_add) * a.t_mul);
+  if (a.lane0_dev) a.lane0 = *a.lane0_dev;
+  const uint64_t first = a.start >> 2;
+  const long long nblk = (long long)(((a.start & 3) + a.n + 3) >> 2);
+  if (tid >= nblk * a.gamma) return;
+  int g = (int)(tid % a.gamma);
+  long long b = tid / a.gamma;
+  uint64_t w[4];
+  philox4x64_10(first + (uint64_t)b + 1ull, a.lane0 + (uint64_t)g, 0ull, 0ull, a.k0, a.k1, w);
+  const double s2 = __dmul_rn(a.sigma, a.sigma);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    long long pos = (long long)((first + (uint64_t)b) * 4ull + (uint64_t)k) - (long long)a.start;
+    if (pos < 0 || pos >= a.n) continue;
+    double gv = ndtri_cephes(word_to_uniform(w[k]));
+    double y = __dadd_rn(1.0, __dmul_rn(a.sigma, gv));
+    if (a.g_lm) a.g_lm[(size_t)g * a.n + pos] = gv;
+    if (a.y_lm) a.y_lm[(size_t)g * a.n + pos] = y;
+    if (a.mu_vm) {
+      double mu = __ddiv_rn(__dmul_rn(2.0, y), s2);
+      mu = mu < -50.0 ? -50.0 : (mu > 50.0 ? 50.0 : mu);
+      a.mu_vm[(size_t)pos * a.gamma + g] = __double2float_rn(mu);
+    }
+  }
+}
+
+}  // namespace
+
+namespace qcb {
+int launch_channel(uint64_t k0, uint64_t k1, uint64_t lane0, uint64_t start, int n, int gamma,
+                   double sigma, float* mu_vm, double* y_lm, double* g_lm, cudaStream_t s) {
+  ChanArgs a{k0, k1, lane0, start, nullptr, nullptr, 0, 0, n, gamma, sigma, mu_vm, y_lm, g_lm};
+  long long nblk = (long long)(((start & 3) + (uint64_t)n + 3) >> 2);
+  long long threads = nblk * gamma;
+  if (threads == 0) return 0;
+  channel_kernel<<<blocks_for(threads), THREADS, 0, s>>>(a);
+  return check_launch("channel");
+}
+// device-indexed variant for graph-captured stream slots: positions start at
+// (*t_dev + t_add) * t_mul, which must be a multiple of 4 (whole Philox blocks).
+int launch_channel_t(uint64_t k0, uint64_t k1, uint64_t lane0, const uint64_t* lane0_dev, uint64_t start,
+                     const int64_t* t_dev, long long t_add, long long t_mul, int n, int gamma, double sigma,
+                     float* mu_vm, cudaStream_t s) {
+  if (!t_dev && !lane0_dev)
+    return launch_channel(k0, k1, lane0, start + (uint64_t)(t_add * t_mul), n, gamma, sigma, mu_vm, nullptr,
+                          nullptr, s);
+  uint64_t st = start;
+  if (!t_dev) st += (uint64_t)(t_add * t_mul);
+  if ((t_dev && t_mul % 4) || st % 4) return fail_arg("device-indexed channel needs 4-aligned starts");
+  ChanArgs a{k0, k1, lane0, st, lane0_dev, t_dev, t_add, t_mul, n, gamma, sigma, mu_vm, nullptr, nullptr};
+  long long threads = (long long)((n + 3) / 4) * gamma;
+  if (threads == 0) return 0;
+  channel_kernel<<<blocks_for(threads), THREADS, 0, s>>>(a);
+  return check_launch("channel");
+}
+}  // namespace qcb
+
+extern "C" int qc_channel(uint64_t seed_lo, uint64_t seed_hi, uint64_t lane0, uint64_t start, int n,
+                          int gamma, double sigma, float* mu_vm, double* y_lm, double* g_lm,
+                          void* stream) {
+  if (n < 0 || gamma < 1) return fail_arg("n must be >= 0 and gamma >= 1");
+  if (mu_vm && gamma % 32) return fail_arg("variable-major mu output needs gamma % 32 == 0");
+  return launch_channel(seed_lo, seed_hi, lane0, start, n, gamma, sigma, mu_vm, y_lm, g_lm,
+                        as_stream(stream));
+}
+
+namespace {
+__global__ void lane_advance_kernel(uint64_t* p, uint64_t k) { *p += k; }
+}
+
+extern "C" int qc_channel_dev(uint64_t seed_lo, uint64_t seed_hi, const uint64_t* lane0_dev, uint64_t start,
+                              int n, int gamma, double sigma, float* mu_vm, void* stream) {
+  if (!lane0_dev || !mu_vm) return fail_arg("null argument");
+  if (n < 0 || gamma < 1 || gamma % 32) return fail_arg("n must be >= 0 and gamma a positive multiple of 32");
+  return launch_channel_t(seed_lo, seed_hi, 0, lane0_dev, start, nullptr, 0, 0, n, gamma, sigma, mu_vm,
+                          as_stream(stream));
+}
+
+extern "C" int qc_lane_advance(uint64_t* lane0_dev, uint64_t k, void* stream) {
+  if (!lane0_dev) return fail_arg("null argument");
+  lane_advance_kernel<<<1, 1, 0, as_stream(stream)>>>(lane0_dev, k);
+  return check_launch("lane_advance");
+}

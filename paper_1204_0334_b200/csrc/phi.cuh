@@ -1,0 +1,57 @@
+// phi(x) = -ln tanh(x/2) = ln((1+e^-x)/(1-e^-x)), x >= 0, in fp32 on the MUFU pipe.
+//
+// The reference evaluates the check rule as 2*atanh(prod tanh(beta/2)) in
+// float64 (bp.py:143-152).  In fp32 that form is unusable (1 - tanh loses all
+// bits above |beta| ~ 8), so the B200 path runs the equivalent log domain
+//   |alpha_k| = min(phi(sum_{j != k} phi(|beta_j|)), ALPHA_CAP),
+//   sign(alpha_k) = prod_{j != k} sign(beta_j),
+// where ALPHA_CAP = 2 atanh(1 - 1e-12) reproduces the reference's tanh-domain
+// clamp (bp.py:150, TANH_CLAMP).  phi is its own inverse.
+//
+// Three branch-free regions, each accurate to a few fp32 ulp relative:
+//   x < 0.25          : m = 1 - e^-x by its Taylor series (expm1 accuracy where
+//                       the subtraction would cancel), phi = ln((2-m)/m)
+//   t = e^-x >= 1/8   : phi = ln((1+t)/(1-t)) via lg2 and rcp
+//   t < 1/8           : phi = 2 atanh(t) = 2t(1 + t^2/3 + t^4/5 + t^6/7)
+//                       (no log: relative accuracy kept for tiny t)
+// m is floored at 1e-30 so phi(0) = 69.3 instead of inf: sums stay finite and
+// the exclusive-sum subtraction can never produce inf - inf.
+#pragma once
+
+namespace qcb {
+
+__device__ __forceinline__ float ex2a(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2a(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcpa(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float phi(float x) {
+  const float LOG2E = 1.4426950408889634f;
+  const float LN2 = 0.6931471805599453f;
+  float t = ex2a(__fmul_rn(-x, LOG2E));
+  float ms = __fmul_rn(
+      x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, -1.0f / 720.0f, 1.0f / 120.0f), -1.0f / 24.0f),
+                              1.0f / 6.0f),
+                      -0.5f),
+              1.0f));
+  float m = (x < 0.25f) ? fmaxf(ms, 1e-30f) : __fsub_rn(1.0f, t);
+  float r = __fmul_rn(__fsub_rn(2.0f, m), rcpa(m));
+  float pl = __fmul_rn(lg2a(r), LN2);
+  float t2 = __fmul_rn(t, t);
+  float ps = __fmul_rn(__fmul_rn(2.0f, t),
+                       fmaf(t2, fmaf(t2, fmaf(t2, 1.0f / 7.0f, 1.0f / 5.0f), 1.0f / 3.0f), 1.0f));
+  return (t < 0.125f) ? ps : pl;
+}
+
+}  // namespace qcb

@@ -1,0 +1,360 @@
+"""Monte-Carlo BER/FER campaigns and throughput benchmarks on B200 GPUs.
+
+Drop-in for /root/reference/pkg/src/qcldpc/harness.py (same config, result
+rows, CSV/JSONL formats, stop rule and lane addressing), with the work moved
+to the device:
+
+* block mode (harness.py:140-204): one launch decodes B reference batches of
+  gamma lanes at once (gamma_kernel = B * gamma).  Channel (Philox + inverse
+  CDF) -> fused init -> 30 flooding iterations -> per-lane bit counts -> per-
+  batch (frames, bit_errors, frame_errors) all run inside one CUDA graph; the
+  host only reads the counter array.  Batch b of point pi draws lanes
+  (pi << 32) + b*gamma + g exactly as the reference, so counts are identical.
+* stream mode (harness.py:212-286): S independent segments decoded side by
+  side (gamma_kernel = S * gamma lanes), every push slot (channel + entry +
+  I check layers + I frames + counting) captured once as a graph.
+* multi-GPU: with a torch.distributed group, round k gives rank r the batches
+  [k*W*B + r*B, k*W*B + (r+1)*B); one all_reduce(SUM) of the int64 per-batch
+  counter array per round; every rank then applies the ordered stop rule.
+  `workers` is accepted for compatibility and ignored (GPUs replace processes).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import json
+import math
+import multiprocessing
+import time
+
+import numpy as np
+
+from . import _lib
+from .bp import BlockDecoder
+from .channel import ebn0_to_sigma, seed_words
+from .codes import EdgeLayout
+from .convolutional import LdpcccCode
+from .dist import ordered_prefix, sum_counts, world
+from .plan import require_cuda
+
+__all__ = [
+    "SimulationConfig", "PointResult", "CSV_COLUMNS", "run_block_simulation",
+    "run_stream_simulation", "bench_throughput", "write_csv", "write_jsonl",
+    "BlockCampaign", "StreamCampaign",
+]
+
+CSV_COLUMNS = [
+    "code_id", "mode", "ebn0_db", "iters_or_I", "gamma", "frames",
+    "bit_errors", "frame_errors", "ber", "fer", "seconds", "frames_per_sec",
+    "info_bits_per_sec",
+]
+TIMING_COLUMNS = ("seconds", "frames_per_sec", "info_bits_per_sec")
+
+
+@dataclasses.dataclass
+class SimulationConfig:
+    """Campaign settings shared by block and stream simulations (harness.py:49-73)."""
+
+    code_id: str
+    ebn0_db: object
+    iterations: int = 30
+    processors: int = 20
+    gamma: int = 32
+    stop_block_errors: int = 100
+    max_frames: int = 1_000_000
+    seed: int = 0
+    workers: int = 1
+    early_stop: bool = False
+    stream_segment_frames: int | None = None
+
+    def points(self) -> list:
+        e = self.ebn0_db
+        return [float(x) for x in (e if isinstance(e, (list, tuple, np.ndarray)) else [e])]
+
+
+@dataclasses.dataclass
+class PointResult:
+    """One CSV row of a campaign."""
+
+    code_id: str
+    mode: str
+    ebn0_db: float
+    iters_or_i: int
+    gamma: int
+    frames: int
+    bit_errors: int
+    frame_errors: int
+    ber: float
+    fer: float
+    seconds: float
+    frames_per_sec: float
+    info_bits_per_sec: float
+
+    def row(self) -> list:
+        return [
+            self.code_id, self.mode, f"{self.ebn0_db:g}", self.iters_or_i,
+            self.gamma, self.frames, self.bit_errors, self.frame_errors,
+            f"{self.ber:.8g}", f"{self.fer:.8g}", f"{self.seconds:.3f}",
+            f"{self.frames_per_sec:.3f}", f"{self.info_bits_per_sec:.3f}",
+        ]
+
+
+def write_csv(results, out) -> None:
+    import csv
+
+    def emit(fh):
+        w = csv.writer(fh)
+        w.writerow(CSV_COLUMNS)
+        for r in results:
+            w.writerow(r.row())
+
+    if hasattr(out, "write"):
+        emit(out)
+    else:
+        with open(out, "w", newline="") as fh:
+            emit(fh)
+
+
+def write_jsonl(records, out) -> None:
+    def emit(fh):
+        for r in records:
+            fh.write(json.dumps(r, sort_keys=True) + "\n")
+
+    if hasattr(out, "write"):
+        emit(out)
+    else:
+        with open(out, "w") as fh:
+            emit(fh)
+
+
+def _kernel_units(gref: int, target_lanes: int, max_units: int) -> int:
+    """Reference batches per launch: a multiple of 32/gcd(gref, 32), ~target_lanes lanes."""
+    step = 32 // math.gcd(gref, 32)
+    want = max(1, min(max_units, -(-target_lanes // gref)))
+    return max(step, -(-want // step) * step)
+
+
+class BlockCampaign:
+    """Device-resident block campaign engine for one code / gamma_kernel / iteration count."""
+
+    def __init__(self, layout: EdgeLayout, gamma_ref: int, units: int, iterations: int,
+                 early_stop: bool, seed: int, graph: bool = True):
+        torch = require_cuda()
+        self.layout, self.gref, self.units = layout, gamma_ref, units
+        self.gk = gamma_ref * units
+        self.k0, self.k1 = seed_words(seed)
+        self.dec = BlockDecoder(layout, self.gk, iterations, early_stop, graph=False, count_bits=True)
+        dev = self.dec.device
+        self.lane0 = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros((units, 3), dtype=torch.int64, device=dev)
+        self.sigma = None
+        self._graph = None
+        self._use_graph = graph
+
+    def _launch(self):
+        n = self.layout.n_vars
+        self.counts.zero_()
+        _lib.call("qc_channel_dev", self.k0, self.k1, self.lane0.data_ptr(), 0, n, self.gk,
+                  float(self.sigma), self.dec.mu.data_ptr(), _lib.stream_handle())
+        self.dec._launch()
+        _lib.call("qc_batch_counts", self.gk, self.gref, self.dec.lane_bits.data_ptr(),
+                  self.counts.data_ptr(), _lib.stream_handle())
+
+    def kernel_launches_per_step(self) -> int:
+        return 1 + self.dec.kernel_launches_per_run() + 1
+
+    def step(self, lane0: int, sigma: float):
+        """Decode lanes lane0 .. lane0 + gamma_kernel - 1; counts -> self.counts (device)."""
+        import torch
+        self.lane0.fill_(int(lane0))
+        if self.sigma != sigma:
+            self.sigma, self._graph = sigma, None
+        if not self._use_graph:
+            self._launch()
+            return
+        if self._graph is None:
+            self._launch()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch()
+            self._graph = g
+            return
+        self._graph.replay()
+
+
+def run_block_simulation(layout: EdgeLayout, config: SimulationConfig, *,
+                         gamma_kernel: int | None = None, group=None) -> list:
+    """Sweep the Eb/N0 points with the GPU block decoder (harness.py:157-204)."""
+    torch = require_cuda()
+    rank, W, g = world() if group is None else (torch.distributed.get_rank(group),
+                                                 torch.distributed.get_world_size(group), group)
+    rate = 1.0 - layout.n_checks / layout.n_vars
+    info_bits = layout.n_vars - layout.n_checks
+    gref = config.gamma
+    max_units = max(1, -(-config.max_frames // (gref * W)))
+    units = _kernel_units(gref, gamma_kernel or 2048, max_units)
+    eng = BlockCampaign(layout, gref, units, config.iterations, config.early_stop, config.seed)
+    results = []
+    for pi, db in enumerate(config.points()):
+        sigma = ebn0_to_sigma(db, rate)
+        lane_base = pi << 32
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tot, done, rnd = (0, 0, 0), False, 0
+        while not done:
+            b0 = (rnd * W + rank) * units
+            eng.step(lane_base + b0 * gref, sigma)
+            allc = torch.zeros((W * units, 3), dtype=torch.int64, device=eng.counts.device)
+            allc[rank * units:(rank + 1) * units] = eng.counts
+            sum_counts(allc, g)
+            tot, done, _ = ordered_prefix(allc.cpu().numpy(), config.stop_block_errors,
+                                          config.max_frames, tot)
+            rnd += 1
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        frames, be, fe = tot
+        results.append(PointResult(
+            code_id=config.code_id, mode="block", ebn0_db=db, iters_or_i=config.iterations,
+            gamma=gref, frames=frames, bit_errors=be, frame_errors=fe,
+            ber=be / (frames * layout.n_vars) if frames else 0.0,
+            fer=fe / frames if frames else 0.0, seconds=dt,
+            frames_per_sec=frames / dt if dt else 0.0,
+            info_bits_per_sec=frames * info_bits / dt if dt else 0.0))
+    return results
+
+
+class StreamCampaign:
+    """Device-resident stream-segment engine: S segments of gamma_ref lanes side by side."""
+
+    def __init__(self, code: LdpcccCode, gamma_ref: int, segments: int, processors: int,
+                 pushes: int, seed: int, graph: bool = True):
+        torch = require_cuda()
+        self.code, self.gref, self.S, self.I, self.pushes = code, gamma_ref, segments, processors, pushes
+        self.gk = gamma_ref * segments
+        self.window = processors * (code.ms + 1)
+        self.k0, self.k1 = seed_words(seed)
+        self.plan = code.plan()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.msg = torch.zeros((processors * code.edge_count, self.gk), dtype=torch.float32, device=dev)
+        self.ring = torch.zeros((self.window, code.c, self.gk), dtype=torch.float32, device=dev)
+        self.mu = torch.zeros((code.c, self.gk), dtype=torch.float32, device=dev)
+        self.cnt = torch.zeros((3, self.gk), dtype=torch.int32, device=dev)
+        self.lane0 = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.sigma = None
+        self._graph = None
+        self._use_graph = graph
+
+    def _launch(self):
+        s = _lib.stream_handle()
+        self.cnt.zero_()
+        for t in range(self.pushes):
+            _lib.call("cc_channel", self.plan.handle, self.k0, self.k1, 0, self.lane0.data_ptr(), t, None,
+                      self.gk, float(self.sigma), self.mu.data_ptr(), s)
+            _lib.call("cc_slot", self.plan.handle, self.I, self.gk, t, None, self.msg.data_ptr(),
+                      self.ring.data_ptr(), self.mu.data_ptr(), None, self.cnt.data_ptr(), s)
+
+    def kernel_launches_per_step(self) -> int:
+        return self.pushes * 5
+
+    def step(self, lane0: int, sigma: float):
+        import torch
+        self.lane0.fill_(int(lane0))
+        if self.sigma != sigma:
+            self.sigma, self._graph = sigma, None
+        if not self._use_graph:
+            self._launch()
+            return
+        if self._graph is None:
+            self._launch()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch()
+            self._graph = g
+            return
+        self._graph.replay()
+
+    def segment_counts(self):
+        """(S, 3) int64 (frames, bit_errors, frame_errors) per segment (device)."""
+        import torch
+        emitted = max(0, self.pushes - self.window + 1)
+        c = self.cnt.view(3, self.S, self.gref).to(torch.int64).sum(dim=2)
+        out = torch.empty((self.S, 3), dtype=torch.int64, device=self.cnt.device)
+        out[:, 0] = emitted * self.gref
+        out[:, 1] = c[1]
+        out[:, 2] = c[2]
+        return out
+
+
+def run_stream_simulation(code: LdpcccCode, config: SimulationConfig, *,
+                          gamma_kernel: int | None = None, group=None) -> list:
+    """Sweep the Eb/N0 points with the GPU pipelined stream decoder (harness.py:236-286)."""
+    torch = require_cuda()
+    rank, W, g = world() if group is None else (torch.distributed.get_rank(group),
+                                                 torch.distributed.get_world_size(group), group)
+    window = config.processors * (code.ms + 1)
+    counted = config.stream_segment_frames or max(2 * (window - 1), 64)
+    pushes = counted + window - 1
+    info_bits = code.c - code.cb
+    gref = config.gamma
+    per_seg = counted * gref
+    max_units = max(1, -(-config.max_frames // (per_seg * W)))
+    units = _kernel_units(gref, gamma_kernel or 256, max_units)
+    eng = StreamCampaign(code, gref, units, config.processors, pushes, config.seed)
+    results = []
+    for pi, db in enumerate(config.points()):
+        sigma = ebn0_to_sigma(db, code.rate_bound)
+        lane_base = pi << 32
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tot, done, rnd = (0, 0, 0), False, 0
+        while not done:
+            s0 = (rnd * W + rank) * units
+            eng.step(lane_base + s0 * gref, sigma)
+            allc = torch.zeros((W * units, 3), dtype=torch.int64, device=eng.cnt.device)
+            allc[rank * units:(rank + 1) * units] = eng.segment_counts()
+            sum_counts(allc, g)
+            tot, done, _ = ordered_prefix(allc.cpu().numpy(), config.stop_block_errors,
+                                          config.max_frames, tot)
+            rnd += 1
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        frames, be, fe = tot
+        results.append(PointResult(
+            code_id=config.code_id, mode="stream", ebn0_db=db, iters_or_i=config.processors,
+            gamma=gref, frames=frames, bit_errors=be, frame_errors=fe,
+            ber=be / (frames * code.c) if frames else 0.0,
+            fer=fe / frames if frames else 0.0, seconds=dt,
+            frames_per_sec=frames / dt if dt else 0.0,
+            info_bits_per_sec=frames * info_bits / dt if dt else 0.0))
+    return results
+
+
+def bench_throughput(layout: EdgeLayout | None, config: SimulationConfig,
+                     code: LdpcccCode | None = None, frames: int = 256) -> list:
+    """Decoded-frames/s records for gamma in {1, config.gamma} (harness.py:294-331).
+
+    `workers` is recorded as in the reference; on the GPU it does not change
+    the execution (one process drives the device)."""
+    cores = multiprocessing.cpu_count()
+    records = []
+    db = config.points()[0]
+    for gamma in sorted({1, config.gamma}):
+        for workers in sorted({1, cores}):
+            cfg = dataclasses.replace(config, gamma=gamma, workers=workers, stop_block_errors=2**62,
+                                      max_frames=frames, ebn0_db=db)
+            if code is not None:
+                res = run_stream_simulation(code, cfg)[0]
+                meta = dict(mode="stream", n=code.c, m=code.cb, edge_count=code.edge_count,
+                            iters_or_I=config.processors)
+            else:
+                res = run_block_simulation(layout, cfg)[0]
+                meta = dict(mode="block", n=layout.n_vars, m=layout.n_checks,
+                            edge_count=layout.edge_count, iters_or_I=config.iterations)
+            records.append(dict(
+                code_id=config.code_id, gamma=gamma, workers=workers, physical_cores=cores,
+                frames=res.frames, seconds=round(res.seconds, 4),
+                frames_per_sec=round(res.frames_per_sec, 3),
+                info_bits_per_sec=round(res.info_bits_per_sec, 1),
+                per_frame_ms=round(1000 * res.seconds / res.frames, 4) if res.frames else None,
+                **meta))
+    return records

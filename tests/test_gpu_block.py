@@ -1,0 +1,203 @@
+"""GPU parity: block decoder kernels vs the oracle / reference goldens.
+
+Tolerance (north star): single message updates |delta| <= 1e-4 * max(|ref|, 1)
+against the float64 reference; decisions, syndromes and error counts bit-exact.
+"""
+import numpy as np
+import pytest
+from conftest import golden
+
+from oracle import bp as obp
+from oracle import channel as och
+from oracle import qc as oqc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def close(got, ref):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    err = np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)
+    assert err.max() <= TOL, f"max scaled error {err.max():.3e}"
+
+
+def toy(q):
+    return q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+
+
+def test_kat_check_update(gpu):
+    q = gpu
+    lay = q.build_edge_layout(q.SparseParityCheck(3, [[0, 1, 2]]))
+    b = q.MessageBatch(lay, np.array([[2.0], [-1.0], [0.5]]))
+    q.check_node_update(b, lay)
+    close(b.packages[:, 0], [-0.22733629380264572863, 0.37747645630979721384, -0.73532566405551922471])
+    lay1 = q.build_edge_layout(q.SparseParityCheck(1, [[0]]))
+    b1 = q.MessageBatch(lay1, np.array([[3.0]]))
+    q.check_node_update(b1, lay1)
+    close(b1.packages[0, 0], 28.324190418452803892)
+    lay2 = q.build_edge_layout(q.SparseParityCheck(2, [[0, 1]]))
+    b2 = q.MessageBatch(lay2, np.array([[1.25], [-0.75]]))
+    q.check_node_update(b2, lay2)
+    close(b2.packages[:, 0], [-0.75, 1.25])
+
+
+def test_single_step_random_degrees(gpu):
+    """One CNU + VNU on identical inputs, degrees 1..32, beta spread up to +-50."""
+    q = gpu
+    rng = np.random.default_rng(1)
+    for d in (1, 2, 3, 4, 5, 6, 7, 8, 11, 12, 16, 20, 24, 31, 32):
+        n = d + 3
+        rows = [sorted(rng.choice(n, size=d, replace=False)) for _ in range(4)]
+        lay = q.build_edge_layout(q.SparseParityCheck(n, rows))
+        olay = oqc.layout_from_rows(n, rows)
+        mu = rng.normal(0, 1, size=(n, 64)) * rng.choice([0.1, 1, 5, 20, 60], size=(n, 1))
+        mu = np.clip(mu, -50, 50).astype(np.float32).astype(np.float64)
+        mu[0, :3] = 0.0
+        b = q.MessageBatch(lay, mu)
+        q.check_node_update(b, lay)
+        ob = obp.init_buffer(olay, mu)
+        obp.check_update(ob, olay)
+        close(b.packages, ob[:-1])
+        # feed identical alphas into the VNU
+        a32 = b.packages.astype(np.float32).astype(np.float64)
+        ob[:-1] = a32
+        post = q.variable_node_update(b, lay)
+        opost = obp.var_update(ob, mu, olay)
+        close(post, opost)
+        close(b.packages, ob[:-1])
+
+
+def test_toy_golden(gpu):
+    q = gpu
+    g = golden("block_toy.npz")
+    lay = toy(q)
+    mu = q.channel_llrs(g["y"], float(g["sigma"]))
+    b = q.MessageBatch(lay, np.ascontiguousarray(mu.T))
+    q.check_node_update(b, lay)
+    close(b.packages, g["cnu1"])
+    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30)
+    assert np.array_equal(r.hard_bits, g["bits30"])
+    assert np.array_equal(r.syndrome_ok, g["ok30"])
+    close(r.posteriors, g["post30"])
+    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30, early_stop=True)
+    assert np.array_equal(r.iterations_run, g["iters_es"])
+    assert np.array_equal(r.syndrome_ok, g["ok_es"])
+    assert np.array_equal(r.hard_bits, g["bits_es"])
+    close(r.posteriors, g["post_es"])
+
+
+@pytest.mark.parametrize("name", ["code_a", "n18360"])
+def test_large_code_golden(gpu, codes_npz, name):
+    """Gamma=32 lanes at the operating point: bits, syndromes, bit errors bit-exact."""
+    q = gpu
+    g = golden(f"block_{name}.npz")
+    exp = q.ExponentMatrix(codes_npz[f"{name}_shifts"], int(codes_npz[f"{name}_p"]))
+    lay = q.build_edge_layout(q.expand_qc(exp))
+    sigma = float(g["sigma"])
+    rate = 1.0 - lay.n_checks / lay.n_vars
+    db = 3.2 if name == "code_a" else 3.0
+    cfg = q.ChannelConfig(db, rate, seed=0, gamma=32)
+    assert cfg.sigma == sigma
+    y = q.simulate_block(cfg, lay.n_vars)               # on-device channel
+    yo = och.received(0, sigma, 0, 32, lay.n_vars)      # oracle channel
+    assert np.abs(y - yo).max() < 1e-12
+    y = yo
+    # single step (lanes 0..3, first edges)
+    mu = q.channel_llrs(y, sigma)
+    b = q.MessageBatch(lay, np.ascontiguousarray(mu.T))
+    q.check_node_update(b, lay)
+    close(b.packages[: g["cnu1_lanes0_3"].shape[0], :4], g["cnu1_lanes0_3"])
+    r = q.decode_batch(lay, y, sigma, 30)
+    assert np.array_equal(np.packbits(r.hard_bits, axis=1), g["bits"])
+    assert np.array_equal(r.syndrome_ok, g["ok"])
+    assert np.array_equal(r.hard_bits.sum(axis=1), g["bit_errors"])
+    conv = g["ok"][:8]
+    close(r.posteriors[:8][conv], g["post8"][conv])
+
+
+def test_wide_batch_matches_single_lane(gpu):
+    q = gpu
+    lay = toy(q)
+    rng = np.random.default_rng(300)
+    for _ in range(20):
+        y = rng.normal(1.0, 1.0, size=(1, lay.n_vars))
+        one = q.decode_batch(lay, y, 1.0, 6)
+        wide = q.decode_batch(lay, np.repeat(y, 32, axis=0), 1.0, 6)
+        assert np.array_equal(np.repeat(one.posteriors, 32, axis=0), wide.posteriors)
+        assert np.array_equal(np.repeat(one.hard_bits, 32, axis=0), wide.hard_bits)
+    # also across kernel variants (gamma 32 / 64 / 128 use VEC 1 / 2 / 4)
+    y = rng.normal(1.0, 1.0, size=(1, lay.n_vars))
+    ref = q.decode_batch(lay, y, 1.0, 9).posteriors
+    for G in (64, 128, 256):
+        w = q.decode_batch(lay, np.repeat(y, G, axis=0), 1.0, 9).posteriors
+        assert np.array_equal(w, np.repeat(ref, G, axis=0))
+
+
+def test_lane_permutation(gpu):
+    q = gpu
+    lay = toy(q)
+    rng = np.random.default_rng(5)
+    y = rng.normal(1.0, 0.9, size=(6, lay.n_vars))
+    perm = rng.permutation(6)
+    r1 = q.decode_batch(lay, y, 0.9, 8)
+    r2 = q.decode_batch(lay, y[perm], 0.9, 8)
+    assert np.array_equal(r1.posteriors[perm], r2.posteriors)
+
+
+def test_irregular_code_against_oracle(gpu):
+    q = gpu
+    rows = [[0, 1, 2, 3, 5, 7, 9], [0, 2, 3, 6, 7, 8, 9], [1, 3, 7], [0, 4, 6, 7, 8, 9], [2, 3, 4, 6, 8]]
+    lay = q.build_edge_layout(q.SparseParityCheck(10, rows))
+    olay = oqc.layout_from_rows(10, rows)
+    rng = np.random.default_rng(8)
+    y = rng.normal(1.0, 0.8, size=(40, 10))
+    r = q.decode_batch(lay, y, 0.8, 10)
+    bits, post, ok, _ = obp.decode_llr(olay, obp.channel_llrs(y, 0.8), 10)
+    assert np.array_equal(r.hard_bits, bits) and np.array_equal(r.syndrome_ok, ok)
+    close(r.posteriors, post)
+    y1 = np.ones((2, 10)); y1[1, 3] = -0.2
+    r = q.decode_batch(lay, y1, 0.6, 10)
+    assert not r.hard_bits.any() and r.syndrome_ok.all()
+
+
+def test_early_stop_semantics(gpu):
+    q = gpu
+    lay = toy(q)
+    rng = np.random.default_rng(13)
+    y = np.ones((8, lay.n_vars))
+    y[4:] = rng.normal(1.0, 1.5, size=(4, lay.n_vars))
+    res = q.decode_batch(lay, y, 0.7, 20, early_stop=True)
+    assert np.all(res.iterations_run[:4] == 1) and res.syndrome_ok[:4].all()
+    r1 = q.decode_batch(lay, y[:4], 0.7, 1)
+    assert np.array_equal(res.posteriors[:4], r1.posteriors)
+    y = rng.normal(1.0, 2.0, size=(6, lay.n_vars))
+    rf = q.decode_batch(lay, y, 2.0, 12)
+    rs = q.decode_batch(lay, y, 2.0, 12, early_stop=True)
+    hard = ~rs.syndrome_ok
+    assert np.all(rs.iterations_run[hard] == 12)
+    assert np.array_equal(rs.posteriors[hard], rf.posteriors[hard])
+    olay = oqc.qc_layout(oqc.array_code_shifts(2, 4, 8), 8)
+    bits, post, ok, its = obp.decode_llr(olay, obp.channel_llrs(y, 2.0), 12, early_stop=True)
+    assert np.array_equal(rs.iterations_run, its) and np.array_equal(rs.syndrome_ok, ok)
+    assert np.array_equal(rs.hard_bits, bits)
+
+
+def test_hard_decision_and_syndrome(gpu):
+    q = gpu
+    lay = q.build_edge_layout(q.SparseParityCheck(3, [[0, 1], [1, 2]]))
+    post = np.array([[1.0, 1.0, 1.0], [-1.0, -1.0, 1.0]]).T
+    bits, ok = q.hard_decision_and_syndrome(lay, post)
+    assert bits[:, 0].tolist() == [0, 0, 0] and ok[0]
+    assert bits[:, 1].tolist() == [1, 1, 0] and not ok[1]
+
+
+def test_decode_errors(gpu):
+    q = gpu
+    lay = toy(q)
+    with pytest.raises(ValueError):
+        q.decode_batch(lay, np.ones((2, lay.n_vars + 1)), 0.8, 5)
+    with pytest.raises(ValueError):
+        q.decode_llr_batch(lay, np.ones((2, lay.n_vars)), 0)
+    r1 = q.decode_batch(lay, np.random.default_rng(2).normal(1, .8, (3, lay.n_vars)), 0.8, 6)
+    r2 = q.decode_llr_batch(lay, q.channel_llrs(np.random.default_rng(2).normal(1, .8, (3, lay.n_vars)), 0.8), 6)
+    assert np.array_equal(r1.posteriors, r2.posteriors)

@@ -1,0 +1,87 @@
+"""GPU campaigns: counts identical to the reference harness (goldens)."""
+import dataclasses
+import io
+import json
+import os
+
+import numpy as np
+import pytest
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+CAMP = json.load(open(os.path.join(GOLDEN, "campaigns.json")))
+
+
+def toy_cfg(q, **kw):
+    base = dict(code_id="toy", ebn0_db=[2.0, 3.0], iterations=8, processors=2, gamma=8,
+                stop_block_errors=15, max_frames=2000, seed=5)
+    base.update(kw)
+    return q.SimulationConfig(**base)
+
+
+def test_toy_block_campaign(gpu):
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    res = q.run_block_simulation(lay, toy_cfg(q))
+    assert [r.row()[:10] for r in res] == CAMP["toy_block"]
+    for gk in (32, 256):
+        res = q.run_block_simulation(lay, toy_cfg(q), gamma_kernel=gk)
+        assert [r.row()[:10] for r in res] == CAMP["toy_block"]
+    buf = io.StringIO()
+    q.write_csv(res, buf)
+    assert buf.getvalue().splitlines()[0].split(",") == q.CSV_COLUMNS
+    r = q.run_block_simulation(lay, toy_cfg(q, stop_block_errors=10**9, max_frames=24))[0]
+    assert r.frames == 24
+
+
+def test_toy_stream_campaign(gpu):
+    q = gpu
+    code = q.unwrap_qc(q.multiplicative_shifts(2, 4, 8))
+    cfg = toy_cfg(q, ebn0_db=[2.0], stop_block_errors=10, max_frames=500, stream_segment_frames=6)
+    res = q.run_stream_simulation(code, cfg)
+    assert [r.row()[:10] for r in res] == CAMP["toy_stream"]
+
+
+def test_code_a_block_256(gpu, codes_npz):
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(q.ExponentMatrix(codes_npz["code_a_shifts"],
+                                                          int(codes_npz["code_a_p"]))))
+    cfg = q.SimulationConfig("code-a", [3.2], iterations=30, gamma=32, stop_block_errors=2**62,
+                             max_frames=256, seed=0)
+    assert [r.row()[:10] for r in q.run_block_simulation(lay, cfg)] == CAMP["code_a_block_256"]
+
+
+def test_recorded_block_campaign(gpu, codes_npz):
+    """pkg/test_output.txt:27 -- 10912 frames / 45450 bit errors / 300 frame errors."""
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(q.ExponentMatrix(codes_npz["code_a_shifts"],
+                                                          int(codes_npz["code_a_p"]))))
+    cfg = q.SimulationConfig("code-a", [3.2], iterations=30, gamma=32, stop_block_errors=300,
+                             max_frames=60_000, seed=0)
+    r = q.run_block_simulation(lay, cfg)[0]
+    want = CAMP["recorded"]["code_a_block_3.2dB_30it_stop300"]
+    assert (r.frames, r.bit_errors, r.frame_errors) == (want["frames"], want["bit_errors"],
+                                                        want["frame_errors"])
+
+
+def test_recorded_stream_campaign(gpu, codes_npz):
+    """pkg/test_output.txt:30 -- 15168 frames / 4627 bit errors / 435 frame errors."""
+    q = gpu
+    code = q.unwrap_qc(q.ExponentMatrix(codes_npz["code_a_shifts"], int(codes_npz["code_a_p"])))
+    cfg = q.SimulationConfig("code-a-stream", [3.1], processors=20, gamma=32,
+                             stop_block_errors=300, max_frames=60_000, seed=0)
+    r = q.run_stream_simulation(code, cfg)[0]
+    want = CAMP["recorded"]["code_a_stream_3.1dB_I20_stop300"]
+    assert (r.frames, r.bit_errors, r.frame_errors) == (want["frames"], want["bit_errors"],
+                                                        want["frame_errors"])
+
+
+def test_bench_records(gpu):
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    recs = q.bench_throughput(lay, toy_cfg(q, ebn0_db=3.0), frames=16)
+    assert {r["gamma"] for r in recs} == {1, 8}
+    assert all(r["frames"] == 16 and r["mode"] == "block" for r in recs)
+    buf = io.StringIO()
+    q.write_jsonl(recs, buf)
+    assert [json.loads(l) for l in buf.getvalue().splitlines()] == recs

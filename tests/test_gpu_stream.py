@@ -1,0 +1,105 @@
+"""GPU parity: pipelined LDPCCC stream decoder vs the reference (goldens) and oracle."""
+import numpy as np
+import pytest
+from conftest import golden
+
+from oracle import qc as oqc
+from oracle import stream as ost
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def close(got, ref):
+    err = np.abs(np.asarray(got) - np.asarray(ref)) / np.maximum(np.abs(ref), 1.0)
+    assert err.max() <= TOL, err.max()
+
+
+def run(q, code, I, G, ys, sigma):
+    dec = q.StreamDecoder(code, I, gamma=G)
+    out = [f for f in (dec.push_frame(y, sigma) for y in ys) if f is not None]
+    return out + dec.flush()
+
+
+def test_stream_small_golden(gpu):
+    q = gpu
+    g = golden("stream_small.npz")
+    code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 8))
+    for I in (2, 3):
+        out = run(q, code, I, 3, g[f"I{I}_ys"], float(g[f"I{I}_sigma"]))
+        assert [f.frame_index for f in out] == g[f"I{I}_index"].tolist()
+        assert [f.tail for f in out] == g[f"I{I}_tail"].tolist()
+        assert np.array_equal(np.stack([f.hard_bits for f in out]), g[f"I{I}_bits"])
+        close(np.stack([f.posteriors for f in out]), g[f"I{I}_post"])
+
+
+def test_stream_code_a_golden(gpu, codes_npz):
+    q = gpu
+    g = golden("stream_code_a.npz")
+    code = q.unwrap_qc(q.ExponentMatrix(codes_npz["code_a_shifts"], int(codes_npz["code_a_p"])))
+    sigma, I, K = float(g["sigma"]), int(g["I"]), int(g["K"])
+    ys = [np.stack([1.0 + sigma * q.lane_normals(0, lane, t * code.c, code.c) for lane in range(2)])
+          for t in range(K)]
+    out = run(q, code, I, 2, ys, sigma)
+    assert [f.frame_index for f in out] == g["index"].tolist()
+    assert [f.tail for f in out] == g["tail"].tolist()
+    assert np.array_equal(np.stack([np.packbits(f.hard_bits, axis=1) for f in out]), g["bits"])
+
+
+def test_stream_vs_oracle_with_zero_blocks(gpu):
+    """Shift grid with -1 blocks exercises the table path of the LDPCCC kernels."""
+    q = gpu
+    rng = np.random.default_rng(9)
+    sh = rng.integers(0, 11, size=(4, 8))
+    sh[0, 1] = sh[2, 5] = sh[3, 3] = -1
+    code = q.unwrap_qc(q.ExponentMatrix(sh, 11))
+    U = oqc.unwrap(sh, 11)
+    sigma, I, G = 0.8, 3, 4
+    ys = rng.normal(1.0, sigma, size=(20, G, code.c))
+    out = run(q, code, I, G, ys, sigma)
+    dec = ost.StreamOracle(U, I, G)
+    ref = [f for f in (dec.push(y, sigma) for y in ys) if f is not None] + dec.flush()
+    assert [f.frame_index for f in out] == [f.frame_index for f in ref]
+    for a, b in zip(out, ref):
+        assert np.array_equal(a.hard_bits, b.hard_bits)
+        close(a.posteriors, b.posteriors)
+
+
+def test_stream_lanes_independent_and_gamma_invariant(gpu):
+    q = gpu
+    code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 8))
+    rng = np.random.default_rng(23)
+    ys = rng.normal(1.0, 1.0, size=(12, 3, code.c))
+    wide = {f.frame_index: f for f in run(q, code, 2, 3, ys, 1.0)}
+    for lane in range(3):
+        single = {f.frame_index: f for f in run(q, code, 2, 1, ys[:, lane:lane + 1], 1.0)}
+        for j in range(12):
+            assert np.array_equal(wide[j].posteriors[lane], single[j].posteriors[0])
+    big = {f.frame_index: f for f in run(q, code, 2, 130, np.repeat(ys[:, :1], 130, axis=1), 1.0)}
+    for j in range(12):
+        assert np.array_equal(big[j].posteriors, np.repeat(wide[j].posteriors[:1], 130, axis=0))
+
+
+def test_stream_api_contract(gpu):
+    q = gpu
+    code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 8))
+    dec = q.StreamDecoder(code, processors=3, gamma=5)
+    assert dec.window == 12
+    assert dec.channel_memory.shape == (12, code.c, 5)
+    assert dec.message_memory.shape == (3, code.edge_count, 5)
+    dec = q.StreamDecoder(code, processors=2)
+    outs = [dec.push_frame(np.ones((1, code.c)), 0.8) for _ in range(8)]
+    assert all(o is None for o in outs[:7]) and outs[7].frame_index == 0 and not outs[7].tail
+    rest = dec.flush()
+    assert [f.frame_index for f in rest] == list(range(1, 8)) and all(f.tail for f in rest)
+    assert not any(f.hard_bits.any() for f in rest)
+    with pytest.raises(RuntimeError):
+        dec.push_frame(np.ones((1, code.c)), 0.8)
+    with pytest.raises(RuntimeError):
+        dec.flush()
+    with pytest.raises(ValueError):
+        q.StreamDecoder(code, processors=0)
+    with pytest.raises(ValueError):
+        q.StreamDecoder(code, 2, gamma=2).push_frame(np.ones((2, code.c + 1)), 0.8)
+    with pytest.raises(ValueError):
+        q.unwrap_qc(q.multiplicative_shifts(3, 5, 7))
