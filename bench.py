@@ -217,19 +217,19 @@ def main():
     st = _lib.stream_handle()
     reps = 20
     for _ in range(3):
-        _lib.call("qc_cnu", dec.plan.handle, dec.gp, dec.msgs.data_ptr(), None, st)
+        _lib.call("qc_cnu_ex", dec.plan.handle, dec.gp, 2, dec.msgs.data_ptr(), dec.mu.data_ptr(), None, st)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        _lib.call("qc_cnu", dec.plan.handle, dec.gp, dec.msgs.data_ptr(), None, st)
+        _lib.call("qc_cnu_ex", dec.plan.handle, dec.gp, 2, dec.msgs.data_ptr(), dec.mu.data_ptr(), None, st)
     e1.record()
     torch.cuda.synchronize()
     cnu_ms = e0.elapsed_time(e1) / reps
     e0.record()
     for _ in range(reps):
-        _lib.call("qc_vnu", dec.plan.handle, dec.gp, dec.msgs.data_ptr(), dec.mu.data_ptr(), None, None,
-                  None, st)
+        _lib.call("qc_vnu_ex", dec.plan.handle, dec.gp, 1, dec.msgs.data_ptr(), dec.mu.data_ptr(), None,
+                  None, None, st)
     e1.record()
     torch.cuda.synchronize()
     vnu_ms = e0.elapsed_time(e1) / reps
@@ -240,7 +240,7 @@ def main():
     step_alg = algorithmic_bytes_per_codeword(E, N, ITERS) * gamma
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "cnu_kernel<24,4,REG> (check-node pass)", "peak_kind": peak_kind,
+                "kernel": "cnu_kernel<24,VEC,REG,CNU_PHI> (check-node pass, phi form)", "peak_kind": peak_kind,
                 "bytes_per_launch": cnu_bytes, "launch_ms": round(cnu_ms, 4),
                 "vnu": {"achieved": round(vnu_bytes / (vnu_ms / 1e3) / 1e9, 1), "launch_ms": round(vnu_ms, 4),
                         "bytes_per_launch": vnu_bytes},

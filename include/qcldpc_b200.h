@@ -67,6 +67,14 @@ QC_API int qc_cnu(const qc_plan* plan, int gamma, float* msgs, const uint32_t* a
  * (post may be NULL); hb (N,gamma/32) hard-bit planes of post (may be NULL). */
 QC_API int qc_vnu(const qc_plan* plan, int gamma, float* msgs, const float* mu, float* post,
            uint32_t* hb, const uint32_t* active, void* stream);
+/* The same passes in the representation used inside qc_decode:
+ * cnu mode 0 = beta in (qc_cnu), 1 = beta^0 gathered from mu (fused init),
+ * 2 = var->check packages hold sign(beta)*phi(|beta|) ("phi form");
+ * vnu mode 0 = write beta (qc_vnu), 1 = write phi form, 2 = no message write. */
+QC_API int qc_cnu_ex(const qc_plan* plan, int gamma, int mode, float* msgs, const float* mu,
+                     const uint32_t* active, void* stream);
+QC_API int qc_vnu_ex(const qc_plan* plan, int gamma, int mode, float* msgs, const float* mu,
+                     float* post, uint32_t* hb, const uint32_t* active, void* stream);
 /* hard_decision_and_syndrome (bp.py:191-210) on hard-bit planes:
  * bad[w] |= lanes of word w with an odd check (bad must be zeroed by caller). */
 QC_API int qc_syndrome(const qc_plan* plan, int gamma, const uint32_t* hb, uint32_t* bad,

@@ -32,6 +32,8 @@ SIGNATURES = {
     "qc_init": (_i, [_p, _i, _p, _p, _p]),
     "qc_cnu": (_i, [_p, _i, _p, _p, _p]),
     "qc_vnu": (_i, [_p, _i, _p, _p, _p, _p, _p, _p]),
+    "qc_cnu_ex": (_i, [_p, _i, _i, _p, _p, _p, _p]),
+    "qc_vnu_ex": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p]),
     "qc_syndrome": (_i, [_p, _i, _p, _p, _p]),
     "qc_hard_bits": (_i, [_p, _i, _p, _p, _p]),
     "qc_bit_errors": (_i, [_p, _i, _p, _p, _p]),

@@ -27,219 +27,11 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
-#include "phi.cuh"
-#include "plan.h"
+#include "block_kernels.cuh"
 
 using namespace qcb;
 
 namespace {
-
-// ----------------------------------------------------------------------------
-// QC arithmetic (regular grid: every block live)
-// edge id of (block row j, circulant row r, block col l) = (j*p + r)*L + l
-// variable of that edge = l*p + (r + s_jl) mod p          (codes.py:159-178)
-// ----------------------------------------------------------------------------
-struct QcGrid {
-  int J, L, p;
-  int16_t s[QC_MAX_J * QC_MAX_L];
-};
-
-__device__ __forceinline__ void stage_grid(const QcGrid& g, int16_t* sh) {
-  for (int i = threadIdx.x; i < g.J * g.L; i += blockDim.x) sh[i] = g.s[i];
-  __syncthreads();
-}
-
-struct CnuArgs {
-  float* msgs;
-  const float* mu;            // FROM_MU: beta^0 gathered from mu (fused init)
-  const int32_t* check_ptr;   // irregular codes
-  const int32_t* edge_var;    // FROM_MU without QC
-  const uint32_t* active;     // lane mask words or null
-  const int32_t* done;        // early-stop "all frozen" flag or null
-  int M, gamma;
-};
-
-// Check-node update on the registers of one thread: x[k][i] = beta of edge k,
-// lane i  ->  alpha.  deg <= DC (pads excluded), lanes not in `lanes` untouched.
-template <int DC, int VEC>
-__device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned lanes) {
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    if (!((lanes >> i) & 1u)) continue;
-    unsigned par = 0;
-    float S = 0.0f, mx = -1.0f;
-    int kmx = 0;
-#pragma unroll
-    for (int k = 0; k < DC; ++k) {
-      if (k < deg) {
-        float b = x[k][i];
-        unsigned sb = __float_as_uint(b) & 0x80000000u;
-        float f = phi(fabsf(b));
-        par ^= sb;
-        if (f > mx) { mx = f; kmx = k; }
-        S = __fadd_rn(S, f);
-        x[k][i] = __uint_as_float(__float_as_uint(f) | sb);   // signed phi
-      }
-    }
-    float S2 = 0.0f;   // exclusive sum of the dominant edge, summed directly
-#pragma unroll
-    for (int k = 0; k < DC; ++k)
-      if (k < deg && k != kmx) S2 = __fadd_rn(S2, fabsf(x[k][i]));
-#pragma unroll
-    for (int k = 0; k < DC; ++k) {
-      if (k < deg) {
-        unsigned u = __float_as_uint(x[k][i]);
-        float f = __uint_as_float(u & 0x7fffffffu);
-        float mag = (k == kmx) ? S2 : __fsub_rn(S, f);
-        float a = fminf(phi(mag), ALPHA_CAP);
-        x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par) & 0x80000000u));
-      }
-    }
-  }
-}
-
-template <int DC, int VEC, bool REG, bool FROM_MU, bool QC>
-__global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid) {
-  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
-  if constexpr (QC && FROM_MU) stage_grid(grid, sh);
-  if (a.done && *a.done) return;
-  const int GV = a.gamma / VEC;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)a.M * GV) return;
-  int m = (int)(tid / GV), q = (int)(tid - (long long)m * GV);
-  int e0, deg;
-  if constexpr (REG) { e0 = m * DC; deg = DC; }
-  else { e0 = a.check_ptr[m]; deg = a.check_ptr[m + 1] - e0; }
-  unsigned lanes = lane_bits_of(a.active, q * VEC, VEC);
-  if (lanes == 0) return;   // frozen lanes keep their packages (bp.py:154-157)
-  float x[DC][VEC];
-  int jrow = 0, r = 0;
-  if constexpr (QC) { jrow = m / grid.p; r = m - jrow * grid.p; }
-#pragma unroll
-  for (int k = 0; k < DC; ++k) {
-    if (k < deg) {
-      if constexpr (FROM_MU) {
-        int v;
-        if constexpr (QC) {
-          int c = r + sh[jrow * grid.L + k];
-          c -= (c >= grid.p) ? grid.p : 0;
-          v = k * grid.p + c;
-        } else {
-          v = a.edge_var[e0 + k];
-        }
-        vload<VEC>(a.mu + (size_t)v * a.gamma + q * VEC, x[k]);
-      } else {
-        vload<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
-      }
-    }
-  }
-  if constexpr (FROM_MU) {
-    // frozen lanes inside the vector must see their stored packages
-    if (lanes != (1u << VEC) - 1u) {
-#pragma unroll
-      for (int k = 0; k < DC; ++k) {
-        if (k < deg) {
-          float old[VEC];
-          vload<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, old);
-#pragma unroll
-          for (int i = 0; i < VEC; ++i)
-            if (!((lanes >> i) & 1u)) x[k][i] = old[i];
-        }
-      }
-    }
-  }
-  cnu_core<DC, VEC>(x, deg, lanes);
-#pragma unroll
-  for (int k = 0; k < DC; ++k)
-    if (k < deg) vstore<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
-}
-
-struct VnuArgs {
-  float* msgs;
-  const float* mu;
-  float* post;               // (N, gamma) or null
-  uint32_t* hb;              // (N, gamma/32) or null
-  const int32_t* var_pad;    // (N, DV) edge ids, -1 pad (non-QC)
-  const uint32_t* active;
-  const int32_t* done;
-  int N, gamma, dv;          // dv = table width
-  int write_beta;
-};
-
-template <int DV, int VEC, bool QC>
-__global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_constant__ QcGrid grid) {
-  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
-  if constexpr (QC) stage_grid(grid, sh);
-  if (a.done && *a.done) return;
-  const int GV = a.gamma / VEC;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  bool valid = tid < (long long)a.N * GV;
-  int n = valid ? (int)(tid / GV) : 0;
-  int q = valid ? (int)(tid - (long long)n * GV) : 0;
-  unsigned lanes = valid ? lane_bits_of(a.active, q * VEC, VEC) : 0u;
-  int e[DV];
-  int deg = 0;
-  if constexpr (QC) {
-    int l = n / grid.p, c = n - l * grid.p;
-#pragma unroll
-    for (int j = 0; j < DV; ++j) {
-      int rr = c - sh[j * grid.L + l];
-      rr += (rr < 0) ? grid.p : 0;
-      e[j] = (j * grid.p + rr) * grid.L + l;
-    }
-    deg = DV;
-  } else {
-#pragma unroll
-    for (int j = 0; j < DV; ++j) {
-      e[j] = (j < a.dv && valid) ? a.var_pad[(size_t)n * a.dv + j] : -1;
-      deg += (e[j] >= 0);
-    }
-  }
-  float tot[VEC], am[DV][VEC];
-  unsigned bits = 0;
-  if (valid && lanes) {
-    vload<VEC>(a.mu + (size_t)n * a.gamma + q * VEC, tot);
-#pragma unroll
-    for (int j = 0; j < DV; ++j)
-      if (j < deg) vload<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, am[j]);
-    // running total in increasing edge order (bp.py:179-181)
-#pragma unroll
-    for (int j = 0; j < DV; ++j)
-      if (j < deg) {
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], am[j][i]);
-      }
-    if (a.write_beta) {
-      const bool all = lanes == (1u << VEC) - 1u;
-#pragma unroll
-      for (int j = 0; j < DV; ++j)
-        if (j < deg) {
-          float b[VEC];
-#pragma unroll
-          for (int i = 0; i < VEC; ++i)
-            b[i] = ((lanes >> i) & 1u) ? clampL(__fsub_rn(tot[i], am[j][i])) : am[j][i];
-          (void)all;
-          vstore<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, b);
-        }
-    }
-    float pst[VEC];
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      pst[i] = clampL(tot[i]);
-      bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
-    }
-    if (a.post) {
-      if (lanes == (1u << VEC) - 1u) {
-        vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
-      } else {
-        for (int i = 0; i < VEC; ++i)
-          if ((lanes >> i) & 1u) a.post[(size_t)n * a.gamma + q * VEC + i] = pst[i];
-      }
-    }
-  }
-  if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, valid);
-}
 
 __global__ void init_kernel(const float* mu, float* msgs, const int32_t* edge_var, int E, int gamma) {
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -414,112 +206,25 @@ __global__ void batch_counts_kernel(const int32_t* lane_bits, int64_t* counts, i
 // dispatch
 // ----------------------------------------------------------------------------
 int bucket_dc(int d) {
-  static const int B[] = {2, 4, 6, 8, 12, 16, 24, 32};
-  for (int b : B)
-    if (d <= b) return b;
-  return -1;
-}
-int bucket_dv(int d) {
-  static const int B[] = {2, 3, 4, 6, 8, 12, 16};
+  static const int B[] = {4, 8, 16, 24, 32};
   for (int b : B)
     if (d <= b) return b;
   return -1;
 }
 
-int pick_vec(int gamma, int dc) {
-  if (dc > 24) return gamma % 64 == 0 ? 2 : 1;
-  if (gamma >= 128) return 4;
-  if (gamma >= 64) return 2;
-  return 1;
-}
-
-QcGrid make_grid(const qc_plan* p) {
-  QcGrid g;
-  std::memset(&g, 0, sizeof(g));
-  if (p->qc_regular) {
-    g.J = p->J; g.L = p->L; g.p = p->p;
-    for (int i = 0; i < p->J * p->L; ++i) g.s[i] = (int16_t)p->shifts[i];
-  }
-  return g;
-}
-
-template <int DC, int VEC>
-void launch_cnu_dv(const qc_plan* p, const CnuArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
-  long long threads = (long long)p->M * (a.gamma / VEC);
-  unsigned nb = blocks_for(threads);
-  const bool reg = p->check_regular == DC;
-  const bool qc = p->qc_regular;
-  if (from_mu) {
-    if (qc && reg) cnu_kernel<DC, VEC, true, true, true><<<nb, THREADS, 0, s>>>(a, g);
-    else if (reg) cnu_kernel<DC, VEC, true, true, false><<<nb, THREADS, 0, s>>>(a, g);
-    else cnu_kernel<DC, VEC, false, true, false><<<nb, THREADS, 0, s>>>(a, g);
-  } else {
-    if (reg) cnu_kernel<DC, VEC, true, false, false><<<nb, THREADS, 0, s>>>(a, g);
-    else cnu_kernel<DC, VEC, false, false, false><<<nb, THREADS, 0, s>>>(a, g);
-  }
-}
-
-template <int DC>
-void launch_cnu_vec(const qc_plan* p, const CnuArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
-  switch (pick_vec(a.gamma, DC)) {
-    case 4: launch_cnu_dv<DC, 4>(p, a, from_mu, g, s); break;
-    case 2: launch_cnu_dv<DC, 2>(p, a, from_mu, g, s); break;
-    default: launch_cnu_dv<DC, 1>(p, a, from_mu, g, s); break;
-  }
-}
-
-int launch_cnu(const qc_plan* p, CnuArgs a, bool from_mu, cudaStream_t s) {
+int launch_cnu(const qc_plan* p, CnuArgs a, int mode, cudaStream_t s) {
   if (p->E == 0 || p->M == 0) return 0;
-  QcGrid g = make_grid(p);
+  int rc;
   switch (bucket_dc(p->dc_max)) {
-    case 2: launch_cnu_vec<2>(p, a, from_mu, g, s); break;
-    case 4: launch_cnu_vec<4>(p, a, from_mu, g, s); break;
-    case 6: launch_cnu_vec<6>(p, a, from_mu, g, s); break;
-    case 8: launch_cnu_vec<8>(p, a, from_mu, g, s); break;
-    case 12: launch_cnu_vec<12>(p, a, from_mu, g, s); break;
-    case 16: launch_cnu_vec<16>(p, a, from_mu, g, s); break;
-    case 24: launch_cnu_vec<24>(p, a, from_mu, g, s); break;
-    case 32: launch_cnu_vec<32>(p, a, from_mu, g, s); break;
+    case 4: rc = launch_cnu_dc<4>(p, a, mode, s); break;
+    case 8: rc = launch_cnu_dc<8>(p, a, mode, s); break;
+    case 16: rc = launch_cnu_dc<16>(p, a, mode, s); break;
+    case 24: rc = launch_cnu_dc<24>(p, a, mode, s); break;
+    case 32: rc = launch_cnu_dc<32>(p, a, mode, s); break;
     default: return fail_arg("check degree > 32 is not supported");
   }
+  if (rc) return rc;
   return check_launch("cnu");
-}
-
-template <int DV, int VEC>
-void launch_vnu_v(const qc_plan* p, const VnuArgs& a, const QcGrid& g, cudaStream_t s) {
-  long long threads = (long long)p->N * (a.gamma / VEC);
-  unsigned nb = blocks_for(threads);
-  if (p->qc_regular && p->J == DV) vnu_kernel<DV, VEC, true><<<nb, THREADS, 0, s>>>(a, g);
-  else vnu_kernel<DV, VEC, false><<<nb, THREADS, 0, s>>>(a, g);
-}
-
-template <int DV>
-void launch_vnu_vec(const qc_plan* p, const VnuArgs& a, const QcGrid& g, cudaStream_t s) {
-  int vec = a.gamma >= 128 ? 4 : (a.gamma >= 64 ? 2 : 1);
-  switch (vec) {
-    case 4: launch_vnu_v<DV, 4>(p, a, g, s); break;
-    case 2: launch_vnu_v<DV, 2>(p, a, g, s); break;
-    default: launch_vnu_v<DV, 1>(p, a, g, s); break;
-  }
-}
-
-int launch_vnu(const qc_plan* p, VnuArgs a, cudaStream_t s) {
-  QcGrid g = make_grid(p);
-  a.var_pad = p->d_var_pad;
-  a.dv = p->dv_max;
-  a.N = p->N;
-  if (p->N == 0) return 0;
-  switch (bucket_dv(std::max(p->dv_max, 1))) {
-    case 2: launch_vnu_vec<2>(p, a, g, s); break;
-    case 3: launch_vnu_vec<3>(p, a, g, s); break;
-    case 4: launch_vnu_vec<4>(p, a, g, s); break;
-    case 6: launch_vnu_vec<6>(p, a, g, s); break;
-    case 8: launch_vnu_vec<8>(p, a, g, s); break;
-    case 12: launch_vnu_vec<12>(p, a, g, s); break;
-    case 16: launch_vnu_vec<16>(p, a, g, s); break;
-    default: return fail_arg("variable degree > 16 is not supported");
-  }
-  return check_launch("vnu");
 }
 
 int check_gamma(int gamma) {
@@ -565,7 +270,7 @@ int qc_cnu(const qc_plan* p, int gamma, float* msgs, const uint32_t* active, voi
   if (int r = check_gamma(gamma)) return r;
   if (!p || !msgs) return fail_arg("null argument");
   CnuArgs a{msgs, nullptr, p->d_check_ptr, p->d_edge_var, active, nullptr, p->M, gamma};
-  return launch_cnu(p, a, false, as_stream(stream));
+  return launch_cnu(p, a, CNU_BETA, as_stream(stream));
 }
 
 int qc_vnu(const qc_plan* p, int gamma, float* msgs, const float* mu, float* post, uint32_t* hb,
@@ -574,8 +279,25 @@ int qc_vnu(const qc_plan* p, int gamma, float* msgs, const float* mu, float* pos
   if (!p || !msgs || !mu) return fail_arg("null argument");
   VnuArgs a{};
   a.msgs = msgs; a.mu = mu; a.post = post; a.hb = hb; a.active = active; a.done = nullptr;
-  a.gamma = gamma; a.write_beta = 1;
-  return launch_vnu(p, a, as_stream(stream));
+  a.gamma = gamma;
+  return launch_vnu(p, a, VNU_BETA, as_stream(stream));
+}
+
+int qc_cnu_ex(const qc_plan* p, int gamma, int mode, float* msgs, const float* mu, const uint32_t* active,
+              void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !msgs || mode < 0 || mode > 2 || (mode == CNU_FROM_MU && !mu)) return fail_arg("bad cnu arguments");
+  CnuArgs a{msgs, mu, p->d_check_ptr, p->d_edge_var, active, nullptr, p->M, gamma};
+  return launch_cnu(p, a, mode, as_stream(stream));
+}
+
+int qc_vnu_ex(const qc_plan* p, int gamma, int mode, float* msgs, const float* mu, float* post, uint32_t* hb,
+              const uint32_t* active, void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (!p || !msgs || !mu || mode < 0 || mode > 2) return fail_arg("bad vnu arguments");
+  VnuArgs a{};
+  a.msgs = msgs; a.mu = mu; a.post = post; a.hb = hb; a.active = active; a.gamma = gamma;
+  return launch_vnu(p, a, mode, as_stream(stream));
 }
 
 int qc_syndrome(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, void* stream) {
@@ -616,35 +338,32 @@ int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const floa
   uint32_t* active = work + W;
   int32_t* done = reinterpret_cast<int32_t*>(work + 2 * W);
   int rc = 0;
+  // Messages between the passes are kept in PHI form (sign * phi(|beta|)):
+  // iteration 1 reads beta^0 = mu straight from the LLRs (fused init).
   if (!early_stop) {
     cudaMemsetAsync(bad, 0, sizeof(uint32_t) * W, s);
     fill_i32<<<blocks_for(gamma), THREADS, 0, s>>>(iters_run, gamma, iters);
     for (int it = 1; it <= iters; ++it) {
       CnuArgs c{msgs, mu, p->d_check_ptr, p->d_edge_var, nullptr, nullptr, p->M, gamma};
-      if ((rc = launch_cnu(p, c, it == 1, s))) return rc;   // iteration 1: init fused (beta^0 = mu)
+      if ((rc = launch_cnu(p, c, it == 1 ? CNU_FROM_MU : CNU_PHI, s))) return rc;
       VnuArgs v{};
       v.msgs = msgs; v.mu = mu; v.gamma = gamma;
-      v.write_beta = it < iters;      // the last beta is never read
       v.post = it == iters ? post : nullptr;
       v.hb = it == iters ? hb : nullptr;
-      if ((rc = launch_vnu(p, v, s))) return rc;
+      if ((rc = launch_vnu(p, v, it < iters ? VNU_PHI : VNU_NONE, s))) return rc;   // last beta never read
     }
     if ((rc = launch_syndrome(p, gamma, hb, bad, nullptr, s))) return rc;
     finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, nullptr, ok, gamma);
   } else {
     es_start_kernel<<<1, 256, 0, s>>>(active, bad, iters_run, done, W, iters);
     for (int it = 1; it <= iters; ++it) {
+      // iteration 1: every lane is active, so the fused init is exact
       CnuArgs c{msgs, mu, p->d_check_ptr, p->d_edge_var, active, done, p->M, gamma};
-      if (it == 1) {
-        // materialise beta^0 so lanes that freeze keep a defined package
-        long long threads = (long long)p->E * (gamma / 4);
-        if (p->E) init_kernel<<<blocks_for(threads), THREADS, 0, s>>>(mu, msgs, p->d_edge_var, p->E, gamma);
-      }
-      if ((rc = launch_cnu(p, c, false, s))) return rc;
+      if ((rc = launch_cnu(p, c, it == 1 ? CNU_FROM_MU : CNU_PHI, s))) return rc;
       VnuArgs v{};
-      v.msgs = msgs; v.mu = mu; v.gamma = gamma; v.write_beta = 1;
+      v.msgs = msgs; v.mu = mu; v.gamma = gamma;
       v.post = post; v.hb = hb; v.active = active; v.done = done;
-      if ((rc = launch_vnu(p, v, s))) return rc;
+      if ((rc = launch_vnu(p, v, VNU_PHI, s))) return rc;
       if ((rc = launch_syndrome(p, gamma, hb, bad, done, s))) return rc;
       es_update_kernel<<<1, 256, 0, s>>>(active, bad, iters_run, done, W, it);
     }

@@ -1,0 +1,242 @@
+// Check- and variable-node kernels of the block decoder (templates).
+//
+// Replaces check_node_update / variable_node_update of
+// /root/reference/pkg/src/qcldpc/bp.py:134-188.  Instantiated per check-degree
+// bucket in cnu_dc*.cu so the many variants compile in parallel.
+//
+// Message representation on the store (edge-major (E, gamma) fp32):
+//   BETA mode (public single-step API): var->check packages hold beta, exactly
+//     the reference's MessageBatch contents (bp.py:59-84).
+//   PHI mode (inside qc_decode): var->check packages hold sign(beta) *
+//     phi(|beta|).  phi is evaluated once by the producer (variable pass) instead
+//     of by the consumer, so each pass evaluates phi once per edge-lane and both
+//     passes stay under the HBM time.
+//   check->var packages always hold alpha.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "phi.cuh"
+#include "plan.h"
+
+namespace qcb {
+
+// regular QC grid (every block live), staged into shared memory per CTA:
+// edge id of (block row j, circulant row r, block col l) = (j*p + r)*L + l,
+// its variable = l*p + (r + s_jl) mod p                      (codes.py:159-178)
+struct QcGrid {
+  int J, L, p;
+  int16_t s[QC_MAX_J * QC_MAX_L];
+};
+
+__device__ __forceinline__ void stage_grid(const QcGrid& g, int16_t* sh) {
+  for (int i = threadIdx.x; i < g.J * g.L; i += blockDim.x) sh[i] = g.s[i];
+  __syncthreads();
+}
+
+enum CnuMode { CNU_BETA = 0, CNU_FROM_MU = 1, CNU_PHI = 2 };
+enum VnuMode { VNU_BETA = 0, VNU_PHI = 1, VNU_NONE = 2 };
+
+struct CnuArgs {
+  float* msgs;
+  const float* mu;            // CNU_FROM_MU: beta^0 gathered from mu (fused init)
+  const int32_t* check_ptr;   // irregular codes
+  const int32_t* edge_var;    // CNU_FROM_MU without QC arithmetic
+  const uint32_t* active;     // lane mask words or null
+  const int32_t* done;        // early-stop "all frozen" flag or null
+  int M, gamma;
+};
+
+struct VnuArgs {
+  float* msgs;
+  const float* mu;
+  float* post;               // (N, gamma) or null
+  uint32_t* hb;              // (N, gamma/32) or null
+  const int32_t* var_pad;    // (N, dv) edge ids, -1 pad (non-QC)
+  const uint32_t* active;
+  const int32_t* done;
+  int N, gamma, dv;
+};
+
+// Check-node update on registers: x[k][i] (edge k, lane i) -> alpha.
+// IN_PHI: inputs are already sign|phi(|beta|); else inputs are beta.
+//   |alpha_k| = min(phi(S - phi_k), ALPHA_CAP), S = sum_k phi_k, except the
+//   dominant edge (largest phi), whose exclusive sum S2 is summed directly so
+//   the subtraction never cancels; sign_k = parity of the other signs.
+template <int DC, int VEC, bool IN_PHI>
+__device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned lanes) {
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    if (!((lanes >> i) & 1u)) continue;
+    unsigned par = 0;
+    float S = 0.0f, mx = -1.0f;
+    int kmx = 0;
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+      if (k < deg) {
+        float b = x[k][i];
+        unsigned sb = __float_as_uint(b) & 0x80000000u;
+        float f = IN_PHI ? fabsf(b) : phi(fabsf(b));
+        par ^= sb;
+        if (f > mx) { mx = f; kmx = k; }
+        S = __fadd_rn(S, f);
+        if (!IN_PHI) x[k][i] = __uint_as_float(__float_as_uint(f) | sb);
+      }
+    }
+    float S2 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < DC; ++k)
+      if (k < deg && k != kmx) S2 = __fadd_rn(S2, fabsf(x[k][i]));
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+      if (k < deg) {
+        unsigned u = __float_as_uint(x[k][i]);
+        float f = __uint_as_float(u & 0x7fffffffu);
+        float mag = (k == kmx) ? S2 : __fsub_rn(S, f);
+        float a = fminf(phi(mag), ALPHA_CAP);
+        x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par) & 0x80000000u));
+      }
+    }
+  }
+}
+
+// one thread = (check m, VEC consecutive lanes); its d_c packages are contiguous
+template <int DC, int VEC, bool REG, int MODE, bool QC>
+__global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid) {
+  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
+  if constexpr (QC && MODE == CNU_FROM_MU) stage_grid(grid, sh);
+  if (a.done && *a.done) return;
+  const int GV = a.gamma / VEC;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)a.M * GV) return;
+  int m = (int)(tid / GV), q = (int)(tid - (long long)m * GV);
+  int e0, deg;
+  if constexpr (REG) { e0 = m * DC; deg = DC; }
+  else { e0 = a.check_ptr[m]; deg = a.check_ptr[m + 1] - e0; }
+  unsigned lanes = lane_bits_of(a.active, q * VEC, VEC);
+  if (lanes == 0) return;   // frozen lanes keep their packages (bp.py:154-157)
+  float x[DC][VEC];
+#pragma unroll
+  for (int k = 0; k < DC; ++k) {
+    if (k < deg) {
+      if constexpr (MODE == CNU_FROM_MU) {
+        int v;
+        if constexpr (QC) {
+          int jrow = m / grid.p, r = m - jrow * grid.p;
+          int c = r + sh[jrow * grid.L + k];
+          c -= (c >= grid.p) ? grid.p : 0;
+          v = k * grid.p + c;
+        } else {
+          v = a.edge_var[e0 + k];
+        }
+        vload<VEC>(a.mu + (size_t)v * a.gamma + q * VEC, x[k]);
+      } else {
+        vload<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
+      }
+    }
+  }
+  cnu_core<DC, VEC, MODE == CNU_PHI>(x, deg, lanes);
+#pragma unroll
+  for (int k = 0; k < DC; ++k)
+    if (k < deg) vstore<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
+}
+
+// one thread = (variable n, VEC consecutive lanes); d_v gathered packages
+template <int DV, int VEC, bool QC, int MODE>
+__global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_constant__ QcGrid grid) {
+  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
+  if constexpr (QC) stage_grid(grid, sh);
+  if (a.done && *a.done) return;
+  const int GV = a.gamma / VEC;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = tid < (long long)a.N * GV;
+  int n = valid ? (int)(tid / GV) : 0;
+  int q = valid ? (int)(tid - (long long)n * GV) : 0;
+  unsigned lanes = valid ? lane_bits_of(a.active, q * VEC, VEC) : 0u;
+  int e[DV];
+  int deg = 0;
+  if constexpr (QC) {
+    int l = n / grid.p, c = n - l * grid.p;
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      int rr = c - sh[j * grid.L + l];
+      rr += (rr < 0) ? grid.p : 0;
+      e[j] = (j * grid.p + rr) * grid.L + l;
+    }
+    deg = DV;
+  } else {
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      e[j] = (j < a.dv && valid) ? a.var_pad[(size_t)n * a.dv + j] : -1;
+      deg += (e[j] >= 0);
+    }
+  }
+  float tot[VEC], am[DV][VEC];
+  unsigned bits = 0;
+  if (valid && lanes) {
+    vload<VEC>(a.mu + (size_t)n * a.gamma + q * VEC, tot);
+#pragma unroll
+    for (int j = 0; j < DV; ++j)
+      if (j < deg) vload<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, am[j]);
+    // running total in increasing edge order (bp.py:179-181)
+#pragma unroll
+    for (int j = 0; j < DV; ++j)
+      if (j < deg) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], am[j][i]);
+      }
+    if constexpr (MODE != VNU_NONE) {
+#pragma unroll
+      for (int j = 0; j < DV; ++j)
+        if (j < deg) {
+          float b[VEC];
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) {
+            float beta = clampL(__fsub_rn(tot[i], am[j][i]));
+            if constexpr (MODE == VNU_PHI)
+              beta = __uint_as_float(__float_as_uint(phi(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+            b[i] = ((lanes >> i) & 1u) ? beta : am[j][i];
+          }
+          vstore<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, b);
+        }
+    }
+    float pst[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      pst[i] = clampL(tot[i]);
+      bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
+    }
+    if (a.post) {
+      if (lanes == (1u << VEC) - 1u) {
+        vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
+      } else {
+        for (int i = 0; i < VEC; ++i)
+          if ((lanes >> i) & 1u) a.post[(size_t)n * a.gamma + q * VEC + i] = pst[i];
+      }
+    }
+  }
+  if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, valid);
+}
+
+// lanes per thread: float4 packages at large gamma, narrower when gamma is
+// small (more threads) or the check degree is large (registers)
+int vec_override();   // QCB_VEC env (tuning experiments); 0 = automatic
+
+inline int pick_vec(int gamma, int dc) {
+  int o = vec_override();
+  if (o == 1 || (o == 2 && gamma % 64 == 0) || (o == 4 && gamma % 128 == 0 && dc <= 24)) return o;
+  if (dc > 24) return gamma % 64 == 0 ? 2 : 1;
+  if (gamma >= 128) return 4;
+  if (gamma >= 64) return 2;
+  return 1;
+}
+
+QcGrid make_grid(const qc_plan* p);
+
+template <int DC>
+int launch_cnu_dc(const qc_plan* p, const CnuArgs& a, int mode, cudaStream_t s);
+
+int launch_vnu(const qc_plan* p, VnuArgs a, int mode, cudaStream_t s);
+
+}  // namespace qcb

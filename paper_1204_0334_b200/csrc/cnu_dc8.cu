@@ -1,0 +1,4 @@
+// Check-node kernels, degree bucket 8 (explicit instantiation unit).
+#include "cnu_launch.cuh"
+
+template int qcb::launch_cnu_dc<8>(const qc_plan*, const qcb::CnuArgs&, int, cudaStream_t);
