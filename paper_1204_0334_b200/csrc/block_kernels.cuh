@@ -60,41 +60,40 @@ struct VnuArgs {
 };
 
 // Check-node update on registers: x[k][i] (edge k, lane i) -> alpha.
-// IN_PHI: inputs are already sign|phi(|beta|); else inputs are beta.
-//   |alpha_k| = min(phi(S - phi_k), ALPHA_CAP), S = sum_k phi_k, except the
-//   dominant edge (largest phi), whose exclusive sum S2 is summed directly so
-//   the subtraction never cancels; sign_k = parity of the other signs.
+// IN_PHI: inputs are sign|psi(|beta|) (psi = phi/ln2); else inputs are beta.
+//   |alpha_k| = min(phi(S - psi_k), ALPHA_CAP), S = sum_k psi_k, except the
+//   dominant edge (largest psi): its exclusive sum S2 is accumulated directly
+//   (S2 = sum of everything but the running maximum), so the subtraction
+//   S - psi_k >= max psi never cancels; sign_k = parity of the other signs.
 template <int DC, int VEC, bool IN_PHI>
 __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned lanes) {
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     if (!((lanes >> i) & 1u)) continue;
     unsigned par = 0;
-    float S = 0.0f, mx = -1.0f;
-    int kmx = 0;
+    float S = 0.0f, S2 = 0.0f, mx = -1.0f;
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
       if (k < deg) {
         float b = x[k][i];
         unsigned sb = __float_as_uint(b) & 0x80000000u;
-        float f = IN_PHI ? fabsf(b) : phi(fabsf(b));
+        float f = IN_PHI ? fabsf(b) : psi_of_nat(fabsf(b));
         par ^= sb;
-        if (f > mx) { mx = f; kmx = k; }
+        S2 = (f > mx) ? S : __fadd_rn(S2, f);
+        mx = fmaxf(mx, f);
         S = __fadd_rn(S, f);
         if (!IN_PHI) x[k][i] = __uint_as_float(__float_as_uint(f) | sb);
       }
     }
-    float S2 = 0.0f;
-#pragma unroll
-    for (int k = 0; k < DC; ++k)
-      if (k < deg && k != kmx) S2 = __fadd_rn(S2, fabsf(x[k][i]));
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
       if (k < deg) {
         unsigned u = __float_as_uint(x[k][i]);
         float f = __uint_as_float(u & 0x7fffffffu);
-        float mag = (k == kmx) ? S2 : __fsub_rn(S, f);
-        float a = fminf(phi(mag), ALPHA_CAP);
+        // S2 excludes the first maximum; an exactly tied maximum has the same
+        // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
+        float mag = (f == mx) ? S2 : __fsub_rn(S, f);
+        float a = fminf(phi_of_log2(mag), ALPHA_CAP);
         x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par) & 0x80000000u));
       }
     }
@@ -195,7 +194,8 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
           for (int i = 0; i < VEC; ++i) {
             float beta = clampL(__fsub_rn(tot[i], am[j][i]));
             if constexpr (MODE == VNU_PHI)
-              beta = __uint_as_float(__float_as_uint(phi(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+              beta = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) |
+                                     (__float_as_uint(beta) & 0x80000000u));
             b[i] = ((lanes >> i) & 1u) ? beta : am[j][i];
           }
           vstore<VEC>(a.msgs + (size_t)e[j] * a.gamma + q * VEC, b);
@@ -223,13 +223,17 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
 // small (more threads) or the check degree is large (registers)
 int vec_override();   // QCB_VEC env (tuning experiments); 0 = automatic
 
-inline int pick_vec(int gamma, int dc) {
+// check pass: 2 lanes per thread (float2) -- measured best on B200 at d_c = 24
+// (4 lanes: 171 registers, 8 warps/SM; 1 lane: LSU-issue bound)
+inline int pick_vec_cnu(int gamma, int dc) {
   int o = vec_override();
   if (o == 1 || (o == 2 && gamma % 64 == 0) || (o == 4 && gamma % 128 == 0 && dc <= 24)) return o;
-  if (dc > 24) return gamma % 64 == 0 ? 2 : 1;
-  if (gamma >= 128) return 4;
-  if (gamma >= 64) return 2;
-  return 1;
+  return gamma % 64 == 0 ? 2 : 1;
+}
+// variable pass: float4 packages
+inline int pick_vec_vnu(int gamma) {
+  if (gamma % 128 == 0) return 4;
+  return gamma % 64 == 0 ? 2 : 1;
 }
 
 QcGrid make_grid(const qc_plan* p);

@@ -96,37 +96,36 @@ __device__ __forceinline__ int var_local(const CcParams& P, const int16_t* sh, c
   }
 }
 
-// generalised check-node core: `present` marks the live positions
+// check-node core with a `present` mask of live positions (bootstrap layers
+// drop absent frames); same arithmetic as the block decoder (block_kernels.cuh)
 template <int DC, int VEC>
 __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long long present) {
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     unsigned par = 0;
-    float S = 0.0f, mx = -1.0f;
-    int kmx = 0;
+    float S = 0.0f, S2 = 0.0f, mx = -1.0f;
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
       if ((present >> k) & 1ull) {
         float b = x[k][i];
         unsigned sb = __float_as_uint(b) & 0x80000000u;
-        float f = phi(fabsf(b));
+        float f = psi_of_nat(fabsf(b));
         par ^= sb;
-        if (f > mx) { mx = f; kmx = k; }
+        S2 = (f > mx) ? S : __fadd_rn(S2, f);
+        mx = fmaxf(mx, f);
         S = __fadd_rn(S, f);
         x[k][i] = __uint_as_float(__float_as_uint(f) | sb);
       }
     }
-    float S2 = 0.0f;
-#pragma unroll
-    for (int k = 0; k < DC; ++k)
-      if (((present >> k) & 1ull) && k != kmx) S2 = __fadd_rn(S2, fabsf(x[k][i]));
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
       if ((present >> k) & 1ull) {
         unsigned u = __float_as_uint(x[k][i]);
         float f = __uint_as_float(u & 0x7fffffffu);
-        float mag = (k == kmx) ? S2 : __fsub_rn(S, f);
-        float al = fminf(phi(mag), ALPHA_CAP);
+        // S2 excludes the first maximum; an exactly tied maximum has the same
+        // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
+        float mag = (f == mx) ? S2 : __fsub_rn(S, f);
+        float al = fminf(phi_of_log2(mag), ALPHA_CAP);
         x[k][i] = __uint_as_float(__float_as_uint(al) | ((u ^ par) & 0x80000000u));
       }
     }

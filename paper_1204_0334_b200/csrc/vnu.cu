@@ -46,7 +46,7 @@ void launch_mode(const qc_plan* p, const VnuArgs& a, int mode, const QcGrid& g, 
 
 template <int DV>
 void launch_vec(const qc_plan* p, const VnuArgs& a, int mode, const QcGrid& g, cudaStream_t s) {
-  int vec = pick_vec(a.gamma, 0);
+  int vec = pick_vec_vnu(a.gamma);
   switch (vec) {
     case 4: launch_mode<DV, 4>(p, a, mode, g, s); break;
     case 2: launch_mode<DV, 2>(p, a, mode, g, s); break;
