@@ -101,6 +101,9 @@ QC_API int qc_decode(const qc_plan* plan, int gamma, int iters, int early_stop, 
  * (either output may be NULL). */
 QC_API int qc_lane_major(int n, int gamma, int gamma_out, const float* post, double* post_out,
                   uint8_t* bits_out, void* stream);
+/* same with an fp32 posterior output (half the device->host bytes) */
+QC_API int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post, float* post_out,
+                             uint8_t* bits_out, void* stream);
 /* lane-major fp64 -> variable-major fp32 LLRs, lanes >= gamma_in padded with +50:
  * sigma > 0: x are received values, mu = clip((2 x)/(sigma sigma), +-50) (channel_llrs, bp.py:54-56);
  * sigma <= 0: x are LLRs, mu = clip(x, +-50) (decode_llr_batch, bp.py:231). */

@@ -40,6 +40,7 @@ SIGNATURES = {
     "qc_decode_work_words": (C.c_size_t, [_i]),
     "qc_decode": (_i, [_p, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "qc_lane_major": (_i, [_i, _i, _i, _p, _p, _p, _p]),
+    "qc_lane_major_f32": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_llr_from_lane_major": (_i, [_i, _i, _i, _p, _d, _p, _p]),
     "qc_channel": (_i, [_u64, _u64, _u64, _u64, _i, _i, _d, _p, _p, _p, _p]),
     "qc_channel_dev": (_i, [_u64, _u64, _p, _u64, _i, _i, _d, _p, _p]),

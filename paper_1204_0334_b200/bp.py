@@ -228,14 +228,17 @@ class BlockDecoder:
         return t
 
     def load_lane_major(self, x: np.ndarray, sigma: float | None):
-        """x (gamma_in, N) fp64: received values (sigma given) or LLRs (sigma None)."""
+        """x (gamma_in, N) fp64: received values (sigma given) or LLRs (sigma None).
+
+        Host side: one multi-threaded copy into a pinned staging buffer, then an
+        async H2D; the LLR scale/clip/transpose runs on the GPU."""
         import torch
         x = np.asarray(x, dtype=np.float64)
         gi, n = x.shape
         if n != self.layout.n_vars or gi > self.gp:
             raise ValueError(f"input {x.shape} does not fit (<= {self.gp}, {self.layout.n_vars})")
         h = self._pinned("x", (gi, n), torch.float64)
-        h.numpy()[...] = x
+        h.copy_(torch.from_numpy(np.ascontiguousarray(x)))
         if self._x is None or tuple(self._x.shape) != (gi, n):
             self._x = torch.empty((gi, n), dtype=torch.float64, device=self.device)
         self._x.copy_(h, non_blocking=True)
@@ -243,21 +246,33 @@ class BlockDecoder:
                   float(sigma) if sigma is not None else 0.0, self.mu.data_ptr(), _stream())
 
     def result(self, gamma: int) -> DecodeResult:
+        """Lane-major results on the host: posteriors leave the GPU as fp32 (the
+        precision they were computed in) and are widened to float64 on the host
+        by a multi-threaded copy; hard bits, syndrome flags, iteration counts."""
         import torch
         n = self.layout.n_vars
-        post_d = torch.empty((gamma, n), dtype=torch.float64, device=self.device)
-        bits_d = torch.empty((gamma, n), dtype=torch.uint8, device=self.device)
-        _lib.call("qc_lane_major", n, self.gp, gamma, self.post.data_ptr(), post_d.data_ptr(),
+        if getattr(self, "_lm", None) is None or self._lm[0].shape[0] != gamma:
+            self._lm = (torch.empty((gamma, n), dtype=torch.float32, device=self.device),
+                        torch.empty((gamma, n), dtype=torch.uint8, device=self.device))
+        post_d, bits_d = self._lm
+        _lib.call("qc_lane_major_f32", n, self.gp, gamma, self.post.data_ptr(), post_d.data_ptr(),
                   bits_d.data_ptr(), _stream())
-        hp = self._pinned("post", (gamma, n), torch.float64)
+        hp = self._pinned("post", (gamma, n), torch.float32)
         hb = self._pinned("bits", (gamma, n), torch.uint8)
+        hs = self._pinned("small", (2, self.gp), torch.int32)
         hp.copy_(post_d, non_blocking=True)
         hb.copy_(bits_d, non_blocking=True)
-        ok = self.ok[:gamma].cpu().numpy().astype(bool)
-        its = self.iters[:gamma].cpu().numpy().astype(np.int64)
+        hs[0].copy_(self.ok.to(torch.int32), non_blocking=True)
+        hs[1].copy_(self.iters, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return DecodeResult(hard_bits=hb.numpy().copy(), posteriors=hp.numpy().copy(),
-                            syndrome_ok=ok, iterations_run=its)
+        post = torch.empty((gamma, n), dtype=torch.float64)
+        post.copy_(hp)
+        bits = torch.empty((gamma, n), dtype=torch.uint8)
+        bits.copy_(hb)
+        small = hs.numpy()
+        return DecodeResult(hard_bits=bits.numpy(), posteriors=post.numpy(),
+                            syndrome_ok=small[0, :gamma].astype(bool),
+                            iterations_run=small[1, :gamma].astype(np.int64))
 
 
 def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool) -> BlockDecoder:

@@ -122,7 +122,11 @@ class StreamDecoder:
 
     @property
     def message_memory(self) -> np.ndarray:
-        """Edge message packages, (I, base edge count, gamma)."""
+        """Edge message packages, (I, base edge count, gamma).
+
+        Internal representation: check->variable packages hold alpha as in the
+        reference; variable->check packages hold sign(beta) * phi(|beta|) / ln 2
+        (the "phi form" the check kernel consumes), not beta itself."""
         m = self._msg[:, : self.gamma].double().cpu().numpy()
         return m.reshape(self.processors, self.code.edge_count, self.gamma)
 

@@ -142,8 +142,9 @@ __global__ void fill_i32(int32_t* p, int n, int v) {
   if (i < n) p[i] = v;
 }
 
-// (N, gamma) fp32 -> (gamma_out, N) fp64 / u8 through a 32x32 smem tile
-__global__ void lane_major_kernel(const float* post, double* post_out, uint8_t* bits_out, int N,
+// (N, gamma) fp32 -> (gamma_out, N) fp64|fp32 / u8 through a 32x32 smem tile
+template <typename OUT>
+__global__ void lane_major_kernel(const float* post, OUT* post_out, uint8_t* bits_out, int N,
                                   int gamma, int gamma_out) {
   __shared__ float tile[32][33];
   int n0 = blockIdx.x * 32, g0 = blockIdx.y * 32;
@@ -156,7 +157,7 @@ __global__ void lane_major_kernel(const float* post, double* post_out, uint8_t* 
     int g = g0 + dy, n = n0 + threadIdx.x;
     if (g < gamma_out && n < N) {
       float v = tile[threadIdx.x][dy];
-      if (post_out) post_out[(size_t)g * N + n] = (double)v;
+      if (post_out) post_out[(size_t)g * N + n] = (OUT)v;
       if (bits_out) bits_out[(size_t)g * N + n] = v < 0.0f ? 1 : 0;
     }
   }
@@ -382,8 +383,18 @@ int qc_lane_major(int n, int gamma, int gamma_out, const float* post, double* po
   if (n < 0 || !post || gamma_out < 0 || gamma_out > gamma) return fail_arg("bad lane_major arguments");
   if (n == 0 || gamma_out == 0) return 0;
   dim3 grid((n + 31) / 32, (gamma_out + 31) / 32), block(32, 8);
-  lane_major_kernel<<<grid, block, 0, as_stream(stream)>>>(post, post_out, bits_out, n, gamma, gamma_out);
+  lane_major_kernel<double><<<grid, block, 0, as_stream(stream)>>>(post, post_out, bits_out, n, gamma, gamma_out);
   return check_launch("lane_major");
+}
+
+int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post, float* post_out, uint8_t* bits_out,
+                      void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (n < 0 || !post || gamma_out < 0 || gamma_out > gamma) return fail_arg("bad lane_major arguments");
+  if (n == 0 || gamma_out == 0) return 0;
+  dim3 grid((n + 31) / 32, (gamma_out + 31) / 32), block(32, 8);
+  lane_major_kernel<float><<<grid, block, 0, as_stream(stream)>>>(post, post_out, bits_out, n, gamma, gamma_out);
+  return check_launch("lane_major_f32");
 }
 
 int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma, float* mu_vm,

@@ -16,6 +16,10 @@
 // memory -- no per-edge tables.  Shift grids with zero blocks fall back to
 // small per-label tables (check (cb, wmax) and variable (c, sub_j) local ids).
 //
+// Message representation: var->check packages hold sign(beta) * psi(|beta|)
+// (phi in log2 units, "phi form", as in the block decoder's loop), check->var
+// packages hold alpha; each pass evaluates phi once per edge-lane.
+//
 // Slot t = three kernels: entry (frame t -> ring + its T sub-blocks), check
 // phase (I layers in one launch: they touch disjoint edge sets), variable
 // phase (I frames, the last one emitted).  The emission-time zero clear of the
@@ -97,7 +101,8 @@ __device__ __forceinline__ int var_local(const CcParams& P, const int16_t* sh, c
 }
 
 // check-node core with a `present` mask of live positions (bootstrap layers
-// drop absent frames); same arithmetic as the block decoder (block_kernels.cuh)
+// drop absent frames); same arithmetic as the block decoder (block_kernels.cuh).
+// Inputs are var->check packages in phi form (sign | psi(|beta|), log2 units).
 template <int DC, int VEC>
 __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long long present) {
 #pragma unroll
@@ -109,12 +114,11 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
       if ((present >> k) & 1ull) {
         float b = x[k][i];
         unsigned sb = __float_as_uint(b) & 0x80000000u;
-        float f = psi_of_nat(fabsf(b));
+        float f = fabsf(b);
         par ^= sb;
         S2 = (f > mx) ? S : __fadd_rn(S2, f);
         mx = fmaxf(mx, f);
         S = __fadd_rn(S, f);
-        x[k][i] = __uint_as_float(__float_as_uint(f) | sb);
       }
     }
 #pragma unroll
@@ -150,6 +154,10 @@ __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid
   }
   const int window = P.I * T;
   vstore<VEC>(a.ring + ((size_t)pmod(t, window) * P.c + v) * P.gamma + q * VEC, m);
+  // beta^0 = mu into the frame's T sub-blocks, stored in phi form
+#pragma unroll
+  for (int i = 0; i < VEC; ++i)
+    m[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(m[i]))) | (__float_as_uint(m[i]) & 0x80000000u));
   const int ph = pmod(t, T);
   const size_t grp = (size_t)pmod(t / T, P.I) * P.E;
   for (int d = 0; d < T; ++d) {
@@ -250,7 +258,10 @@ __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_c
       if ((present >> k) & 1u) {
         float b[VEC];
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) b[i] = clampL(__fsub_rn(tot[i], am[k][i]));
+        for (int i = 0; i < VEC; ++i) {
+          float beta = clampL(__fsub_rn(tot[i], am[k][i]));   // stored in phi form
+          b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+        }
         vstore<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, b);
       }
   } else {
