@@ -151,12 +151,61 @@ def run_reference(args):
     }), flush=True)
 
 
+def stream_bench(args, q, rank, W, group, barrier):
+    """BASELINE configs[2]: LDPCCC unwrapped from the n18360 grid (18360', T = 4,
+    c = 4590, b = 3825), I = 20 processors, harness segments (counted =
+    2(window-1) frames, pushes = counted + window - 1), 3.1 dB, gamma lanes
+    (gamma/32 reference segments side by side), every slot on the GPU
+    (channel, entry, I check layers, I frames, counters) replayed as one graph."""
+    import torch
+    from paper_1204_0334_b200.dist import max_scalar
+    h, exp = q.load_code(q.codes.bundled_code_path("n18360"))
+    code = q.unwrap_qc(exp)
+    I = 20
+    window = I * (code.ms + 1)
+    counted = max(2 * (window - 1), 64)
+    pushes = counted + window - 1
+    G = args.stream_gamma
+    sigma = q.ebn0_to_sigma(3.1, code.rate_bound)
+    eng = q.StreamCampaign(code, 32, G // 32, I, pushes, seed=0)
+    eng.step((rank * 1000) * G, sigma)          # eager warm-up + graph capture
+    eng.step((rank * 1000 + 1) * G, sigma)
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for s in range(args.stream_steps):
+        eng.step((rank * 1000 + 2 + s) * G, sigma)
+    b.record()
+    barrier()
+    ms = max_scalar(a.elapsed_time(b), group, device="cuda") / args.stream_steps
+    frames = counted * G * W
+    E, c, lam = code.edge_count, code.c, code.lam
+    slot_bytes = 4 * (4 * I * E // lam + (I + 1) * c)          # SURVEY 8(d), per lane per slot
+    alg = slot_bytes * G * pushes
+    peak, _ = load_peaks()
+    counts = eng.segment_counts().cpu().numpy()
+    return {"metric": "LDPCCC decoded info Mbit/s (I=20 window decoder, harness segments)",
+            "value": round(frames * (c - code.cb) / (ms / 1e3) / 1e6, 2), "unit": "Mbit/s",
+            "ms_per_step": round(ms, 3),
+            "config": {"code": "18360' (n18360 grid unwrapped, T=4, c=4590, b=3825)", "I": I,
+                       "gamma": G, "segments": G // 32, "pushes": pushes, "counted_frames": counted,
+                       "ebn0_db": 3.1},
+            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
+                         "alg_bytes_per_lane_slot": slot_bytes},
+            "steady_state_mbit_s_at_roofline": round(peak * 1e9 / slot_bytes * (c - code.cb) / 1e6, 1),
+            "gpu_launches_per_step": eng.kernel_launches_per_step(),
+            "frame_errors_last_step": int(counts[:, 2].sum())}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--gamma", type=int, default=2048)
+    ap.add_argument("--gamma", type=int, default=4096)
+    ap.add_argument("--stream-gamma", type=int, default=256, help="lanes of the LDPCCC measurement (0 = skip)")
+    ap.add_argument("--stream-steps", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-batches", type=int, default=0, help="cpu_baseline sample size (0 = cores)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -266,9 +315,11 @@ def main():
         dt = max_scalar(time.perf_counter() - t0, group, device="cuda")
         e2e = {"value": round(e_steps * gamma * W * K_info / dt / 1e6, 2), "unit": "Mbit/s",
                "h2d_bytes_per_step": gamma * N * 8,
-               "d2h_bytes_per_step": gamma * N * 8 + gamma * N + gamma * 1 + gamma * 4,
+               "d2h_bytes_per_step": gamma * N * 4 + gamma * N + 2 * gamma * 4,
                "api": "paper_1204_0334_b200.decode_batch (numpy in, DecodeResult out)"}
         del och
+
+    stream = stream_bench(args, q, rank, W, group, barrier) if args.stream_gamma else None
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -291,6 +342,7 @@ def main():
                        "l2": f"message store {E * gamma * 4 / 1e6:.0f} MB vs 126 MB L2 (inputs larger than L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": eng.kernel_launches_per_step() * args.steps,
+            "stream": stream,
             "clocks": ck,
             "frame_errors_last_step": int(counts[:, 2].sum()),
         }), flush=True)

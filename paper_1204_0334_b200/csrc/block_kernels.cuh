@@ -101,8 +101,11 @@ __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned 
 }
 
 // one thread = (check m, VEC consecutive lanes); its d_c packages are contiguous
-template <int DC, int VEC, bool REG, int MODE, bool QC, int MINB = 1>
-__global__ void __launch_bounds__(THREADS, MINB) cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid) {
+// note: a bare __launch_bounds__(256) gives 128 registers at d_c=24/float2
+// (16 warps/SM, measured best); an explicit min-blocks of 1 lets ptxas grow to
+// 188, and 3 forces spills -- both measured slower on B200.
+template <int DC, int VEC, bool REG, int MODE, bool QC>
+__global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid) {
   __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
   if constexpr (QC && MODE == CNU_FROM_MU) stage_grid(grid, sh);
   if (a.done && *a.done) return;
@@ -142,8 +145,8 @@ __global__ void __launch_bounds__(THREADS, MINB) cnu_kernel(CnuArgs a, const __g
 }
 
 // one thread = (variable n, VEC consecutive lanes); d_v gathered packages
-template <int DV, int VEC, bool QC, int MODE, int MINB = 1>
-__global__ void __launch_bounds__(THREADS, MINB) vnu_kernel(VnuArgs a, const __grid_constant__ QcGrid grid) {
+template <int DV, int VEC, bool QC, int MODE>
+__global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_constant__ QcGrid grid) {
   __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
   if constexpr (QC) stage_grid(grid, sh);
   if (a.done && *a.done) return;
@@ -222,7 +225,6 @@ __global__ void __launch_bounds__(THREADS, MINB) vnu_kernel(VnuArgs a, const __g
 // lanes per thread: float4 packages at large gamma, narrower when gamma is
 // small (more threads) or the check degree is large (registers)
 int vec_override();   // QCB_VEC env (tuning experiments); 0 = automatic
-int minb_override();  // QCB_MINB env: launch-bounds variant of the phi-form passes
 
 // check pass: 2 lanes per thread (float2) -- measured best on B200 at d_c = 24
 // (4 lanes: 171 registers, 8 warps/SM; 1 lane: LSU-issue bound)

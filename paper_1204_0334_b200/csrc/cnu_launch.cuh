@@ -19,10 +19,6 @@ int launch_cnu_v(const qc_plan* p, const CnuArgs& a, int mode, cudaStream_t s) {
       else cnu_kernel<DC, VEC, false, CNU_FROM_MU, false><<<nb, THREADS, 0, s>>>(a, g);
       break;
     case CNU_PHI:
-      if constexpr (VEC == 2) {
-        if (reg && minb_override() == 3) { cnu_kernel<DC, VEC, true, CNU_PHI, false, 3><<<nb, THREADS, 0, s>>>(a, g); break; }
-        if (reg && minb_override() == 4) { cnu_kernel<DC, VEC, true, CNU_PHI, false, 4><<<nb, THREADS, 0, s>>>(a, g); break; }
-      }
       if (reg) cnu_kernel<DC, VEC, true, CNU_PHI, false><<<nb, THREADS, 0, s>>>(a, g);
       else cnu_kernel<DC, VEC, false, CNU_PHI, false><<<nb, THREADS, 0, s>>>(a, g);
       break;

@@ -7,14 +7,6 @@
 
 namespace qcb {
 
-int minb_override() {
-  static int v = [] {
-    const char* e = std::getenv("QCB_MINB");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 int vec_override() {
   static int v = [] {
     const char* e = std::getenv("QCB_VEC");
@@ -39,10 +31,6 @@ template <int DV, int VEC, int MODE>
 void launch_v(const qc_plan* p, const VnuArgs& a, const QcGrid& g, cudaStream_t s) {
   long long threads = (long long)p->N * (a.gamma / VEC);
   unsigned nb = blocks_for(threads);
-  if constexpr (MODE == VNU_PHI && VEC == 4) {
-    if (p->qc_regular && p->J == DV && minb_override() == 3) { vnu_kernel<DV, VEC, true, MODE, 6><<<nb, THREADS, 0, s>>>(a, g); return; }
-    if (p->qc_regular && p->J == DV && minb_override() == 4) { vnu_kernel<DV, VEC, true, MODE, 8><<<nb, THREADS, 0, s>>>(a, g); return; }
-  }
   if (p->qc_regular && p->J == DV) vnu_kernel<DV, VEC, true, MODE><<<nb, THREADS, 0, s>>>(a, g);
   else vnu_kernel<DV, VEC, false, MODE><<<nb, THREADS, 0, s>>>(a, g);
 }
