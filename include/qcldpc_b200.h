@@ -144,12 +144,16 @@ QC_API int cc_plan_dims(const cc_plan* plan, int64_t* dims);
  *   ring  (I*(ms+1), c, gamma) fp32 channel-LLR ring,
  *   mu_in (c, gamma) fp32 LLRs of frame t (NULL = zero-LLR virtual frame, flush),
  *   post_out (c, gamma) fp32 posterior of the emitted frame t-I(ms+1)+1 (may be NULL),
- *   lane_cnt (3, gamma) i32 (may be NULL): row 0 scratch, row 1 += bit errors,
- *   row 2 += frame errors of every emitted frame (harness.py:228-232).
+ *   lane_cnt (3, gamma) i32 (may be NULL): row 0 = bit count of the frame emitted
+ *   by the previous slot (folded by the next slot's entry kernel), row 1 += bit
+ *   errors, row 2 += frame errors of every emitted frame (harness.py:228-232);
+ *   call cc_fold after the last slot of a segment.
  * t_dev: if non-NULL the slot index is *t_dev + t (device-resident slot
  * counter, so a CUDA graph of K slots can be replayed; see cc_advance). */
 QC_API int cc_slot(const cc_plan* plan, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg,
             float* ring, const float* mu_in, float* post_out, int32_t* lane_cnt, void* stream);
+/* fold the last emitted frame's count into lane_cnt rows 1-2 (end of segment) */
+QC_API int cc_fold(int32_t* lane_cnt, int gamma, void* stream);
 /* *t_dev += k (ends a graph of k slots). */
 QC_API int cc_advance(int64_t* t_dev, int64_t k, void* stream);
 /* Channel for stream segments: frame t of lanes lane0.. at positions t*c

@@ -73,8 +73,8 @@ int launch_channel(uint64_t k0, uint64_t k1, uint64_t lane0, uint64_t start, int
   channel_kernel<<<blocks_for(threads), THREADS, 0, s>>>(a);
   return check_launch("channel");
 }
-// device-indexed variant for graph-captured stream slots: positions start at
-// (*t_dev + t_add) * t_mul, which must be a multiple of 4 (whole Philox blocks).
+// device-indexed variant for graph-captured slots: positions start at
+// start + (*t_dev + t_add) * t_mul and/or the first lane is *lane0_dev.
 int launch_channel_t(uint64_t k0, uint64_t k1, uint64_t lane0, const uint64_t* lane0_dev, uint64_t start,
                      const int64_t* t_dev, long long t_add, long long t_mul, int n, int gamma, double sigma,
                      float* mu_vm, cudaStream_t s) {
@@ -83,9 +83,9 @@ int launch_channel_t(uint64_t k0, uint64_t k1, uint64_t lane0, const uint64_t* l
                           nullptr, s);
   uint64_t st = start;
   if (!t_dev) st += (uint64_t)(t_add * t_mul);
-  if ((t_dev && t_mul % 4) || st % 4) return fail_arg("device-indexed channel needs 4-aligned starts");
   ChanArgs a{k0, k1, lane0, st, lane0_dev, t_dev, t_add, t_mul, n, gamma, sigma, mu_vm, nullptr, nullptr};
-  long long threads = (long long)((n + 3) / 4) * gamma;
+  // the start may be known only on the device: cover the worst-case block count
+  long long threads = (long long)((n + 3) / 4 + 1) * gamma;
   if (threads == 0) return 0;
   channel_kernel<<<blocks_for(threads), THREADS, 0, s>>>(a);
   return check_launch("channel");

@@ -68,16 +68,17 @@ struct SlotArgs {
   const int32_t* check_tab;
   const int32_t* var_tab;
   const int64_t* t_dev;
-  long long t;              // slot (t_dev: offset added to *t_dev)
+  int t;                    // slot (t_dev: offset added to *t_dev); < 2^31
 };
 
-__device__ __forceinline__ long long slot_of(const SlotArgs& a) {
-  return a.t_dev ? (*a.t_dev + a.t) : a.t;
+__device__ __forceinline__ int slot_of(const SlotArgs& a) {
+  return a.t_dev ? (int)(*a.t_dev) + a.t : a.t;
 }
 
-__device__ __forceinline__ int pmod(long long x, int m) {
-  long long r = x % m;
-  return (int)(r < 0 ? r + m : r);
+// x mod m for x >= -m*k (slot arithmetic stays in 32 bits)
+__device__ __forceinline__ int pmod(int x, int m) {
+  int r = x % m;
+  return r < 0 ? r + m : r;
 }
 
 __device__ __forceinline__ void stage(const CcParams& P, int16_t* sh) {
@@ -85,19 +86,36 @@ __device__ __forceinline__ void stage(const CcParams& P, int16_t* sh) {
   __syncthreads();
 }
 
-// local edge id of (variable v of a frame, block row br) inside sub-block `lbl`
-template <bool QC>
-__device__ __forceinline__ int var_local(const CcParams& P, const int16_t* sh, const int32_t* var_tab,
-                                         int lbl, int v, int br) {
-  if constexpr (QC) {
-    int bc = v / P.p, cc = v - bc * P.p;
-    int R = lbl / P.lam, Cc = lbl - R * P.lam;
-    int rr = cc - sh[(R * P.sj + br) * P.L + Cc * P.sl + bc];
-    rr += rr < 0 ? P.p : 0;
-    return (br * P.p + rr) * P.sl + bc;
-  } else {
-    return var_tab[((size_t)lbl * P.c + v) * P.sj + br];
+// Edges of variable v (block column bc, circulant column cc) of a frame with
+// phase ph in group base `grp`, in the reference's summation order
+// (d = 0..T-1 over LUT_v[ph][d], then block row br; convolutional.py:414-423).
+// QC: local id of (br, bc) in sub-block (R, ph) = (br*p + (cc - s) mod p)*sl + bc.
+template <int DV, bool QC>
+__device__ __forceinline__ unsigned var_edges(const CcParams& P, const int16_t* sh, const int32_t* var_tab,
+                                              int ph, unsigned grp, int v, int bc, int cc, unsigned (&e)[DV]) {
+  unsigned present = 0;
+  const int T = P.lam;
+  int d = 0, br = 0;
+#pragma unroll
+  for (int k = 0; k < DV; ++k) {
+    e[k] = 0;
+    if (k < T * P.sj) {
+      int R = ph + d;
+      R -= (R >= T) ? T : 0;
+      int lbl = R * T + ph;
+      int loc;
+      if constexpr (QC) {
+        int rr = cc - sh[(R * P.sj + br) * P.L + ph * P.sl + bc];
+        rr += rr < 0 ? P.p : 0;
+        loc = (br * P.p + rr) * P.sl + bc;
+      } else {
+        loc = var_tab[((size_t)lbl * P.c + v) * P.sj + br];
+      }
+      if (loc >= 0) { e[k] = grp + (unsigned)P.sub_off[lbl] + (unsigned)loc; present |= 1u << k; }
+      if (++br == P.sj) { br = 0; ++d; }
+    }
   }
+  return present;
 }
 
 // check-node core with a `present` mask of live positions (bootstrap layers
@@ -136,14 +154,22 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
   }
 }
 
-// ---- entry: frame t into ring slot t mod window and its T sub-blocks -------
-template <int VEC, bool QC>
+// ---- entry: frame t into ring slot t mod window and its T sub-blocks --------
+// Also folds the previous slot's emitted-frame bit count into the lane counters.
+template <int DV, int VEC, bool QC>
 __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   __shared__ int16_t sh[CC_MAX_SHIFTS];
   if constexpr (QC) stage(P, sh);
-  const long long t = slot_of(a);
-  const int T = P.lam, GV = P.gamma / VEC;
+  const int t = slot_of(a);
+  const int T = P.lam, GV = P.gamma / VEC, window = P.I * T;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.cnt && t >= window && tid < P.gamma) {   // previous slot emitted a frame
+    int g = (int)tid;
+    int b = a.cnt[g];
+    a.cnt[P.gamma + g] += b;
+    a.cnt[2 * P.gamma + g] += b > 0;
+    a.cnt[g] = 0;
+  }
   if (tid >= (long long)P.c * GV) return;
   int v = (int)(tid / GV), q = (int)(tid - (long long)v * GV);
   float m[VEC];
@@ -152,54 +178,58 @@ __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid
 #pragma unroll
     for (int i = 0; i < VEC; ++i) m[i] = 0.0f;
   }
-  const int window = P.I * T;
   vstore<VEC>(a.ring + ((size_t)pmod(t, window) * P.c + v) * P.gamma + q * VEC, m);
   // beta^0 = mu into the frame's T sub-blocks, stored in phi form
 #pragma unroll
   for (int i = 0; i < VEC; ++i)
     m[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(m[i]))) | (__float_as_uint(m[i]) & 0x80000000u));
-  const int ph = pmod(t, T);
-  const size_t grp = (size_t)pmod(t / T, P.I) * P.E;
-  for (int d = 0; d < T; ++d) {
-    int lbl = ((ph + d) % T) * T + ph;
-    for (int br = 0; br < P.sj; ++br) {
-      int loc = var_local<QC>(P, sh, a.var_tab, lbl, v, br);
-      if (loc >= 0) vstore<VEC>(a.msg + (grp + P.sub_off[lbl] + loc) * P.gamma + q * VEC, m);
-    }
-  }
+  const int bc = v / P.p, cc = v - bc * P.p;
+  unsigned e[DV];
+  unsigned present = var_edges<DV, QC>(P, sh, a.var_tab, pmod(t, T), (unsigned)pmod(t / T, P.I) * (unsigned)P.E,
+                                        v, bc, cc, e);
+#pragma unroll
+  for (int k = 0; k < DV; ++k)
+    if ((present >> k) & 1u) vstore<VEC>(a.msg + (size_t)e[k] * P.gamma + q * VEC, m);
 }
 
-// ---- check phase: processors i = 1..I refresh layer s = t - (i-1)T --------
+// ---- check phase: processors i = 1..I refresh layer s = t - (i-1)T ---------
 template <int DC, int VEC, bool QC>
 __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
-  const long long t = slot_of(a);
+  const int t = slot_of(a);
   const int T = P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)P.I * P.cb * GV) return;
   int ip = (int)(tid / ((long long)P.cb * GV));
-  long long rem = tid - (long long)ip * P.cb * GV;
-  int r = (int)(rem / GV), q = (int)(rem - (long long)r * GV);
-  const long long s = t - (long long)ip * T;
+  int rem = (int)(tid - (long long)ip * P.cb * GV);
+  int r = rem / GV, q = rem - r * GV;
+  const int s = t - ip * T;
   if (s < 0) return;
   const int kap = pmod(s, T);
   const int W = QC ? P.sl : P.wmax;
   unsigned eidx[DC];   // package index (I*E < 2^32)
   unsigned long long present = 0;
+  // walk d = 0..T-1 (frames s-ms+d, oldest first) and w = 0..W-1 incrementally
+  int d = 0, w = 0;
+  int f = s - P.ms;
+  int lbl = kap * T + (kap + 1 < T ? kap + 1 : kap + 1 - T);
+  unsigned base = f >= 0 ? (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] : 0u;
 #pragma unroll
-  for (int k = 0; k < DC; ++k) eidx[k] = 0;
-  for (int d = 0; d < T; ++d) {
-    long long f = s - P.ms + d;
-    if (f < 0) continue;   // bootstrap: absent frames drop out (convolutional.py:276-279)
-    int lbl = kap * T + (kap + 1 + d) % T;
-    unsigned base = (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl];
-#pragma unroll
-    for (int k = 0; k < DC; ++k) {
-      if (k / W == d) {
-        int w = k - d * W;
+  for (int k = 0; k < DC; ++k) {
+    eidx[k] = 0;
+    if (k < T * W) {
+      if (f >= 0) {   // bootstrap: absent frames drop out (convolutional.py:276-279)
         int loc;
         if constexpr (QC) loc = r * P.sl + w;
         else loc = a.check_tab[((size_t)lbl * P.cb + r) * P.wmax + w];
-        if (loc >= 0) { eidx[k] = base + loc; present |= 1ull << k; }
+        if (loc >= 0) { eidx[k] = base + (unsigned)loc; present |= 1ull << k; }
+      }
+      if (++w == W) {
+        w = 0; ++d; ++f;
+        int c2 = kap + 1 + d;
+        c2 -= (c2 >= T) ? T : 0;
+        c2 -= (c2 >= T) ? T : 0;
+        lbl = kap * T + c2;
+        base = f >= 0 ? (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] : 0u;
       }
     }
   }
@@ -213,39 +243,29 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
     if ((present >> k) & 1ull) vstore<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
 }
 
-// ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 -----
+// ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 ------
 template <int DV, int VEC, bool QC>
 __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   __shared__ int16_t sh[CC_MAX_SHIFTS];
   if constexpr (QC) stage(P, sh);
-  const long long t = slot_of(a);
+  const int t = slot_of(a);
   const int T = P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)P.I * P.c * GV) return;
   int ip = (int)(tid / ((long long)P.c * GV));
-  long long rem = tid - (long long)ip * P.c * GV;
-  int v = (int)(rem / GV), q = (int)(rem - (long long)v * GV);
-  const long long j = t - (long long)(ip + 1) * T + 1;
+  int rem = (int)(tid - (long long)ip * P.c * GV);
+  int v = rem / GV, q = rem - v * GV;
+  const int j = t - (ip + 1) * T + 1;
   if (j < 0) return;
-  const int pj = pmod(j, T);
-  const unsigned grp = (unsigned)pmod(j / T, P.I) * (unsigned)P.E;
-  unsigned eidx[DV];
-  unsigned present = 0;
-#pragma unroll
-  for (int k = 0; k < DV; ++k) {
-    eidx[k] = 0;
-    int d = k / P.sj, br = k - d * P.sj;
-    if (d < T) {
-      int lbl = ((pj + d) % T) * T + pj;
-      int loc = var_local<QC>(P, sh, a.var_tab, lbl, v, br);
-      if (loc >= 0) { eidx[k] = grp + P.sub_off[lbl] + loc; present |= 1u << k; }
-    }
-  }
+  const int bc = v / P.p, cc = v - bc * P.p;
+  unsigned e[DV];
+  unsigned present = var_edges<DV, QC>(P, sh, a.var_tab, pmod(j, T), (unsigned)pmod(j / T, P.I) * (unsigned)P.E,
+                                        v, bc, cc, e);
   float tot[VEC], am[DV][VEC];
   vload<VEC>(a.ring + ((size_t)pmod(j, P.I * T) * P.c + v) * P.gamma + q * VEC, tot);
 #pragma unroll
   for (int k = 0; k < DV; ++k)
-    if ((present >> k) & 1u) vload<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, am[k]);
+    if ((present >> k) & 1u) vload<VEC>(a.msg + (size_t)e[k] * P.gamma + q * VEC, am[k]);
 #pragma unroll
   for (int k = 0; k < DV; ++k)
     if ((present >> k) & 1u) {
@@ -262,7 +282,7 @@ __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_c
           float beta = clampL(__fsub_rn(tot[i], am[k][i]));   // stored in phi form
           b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
         }
-        vstore<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, b);
+        vstore<VEC>(a.msg + (size_t)e[k] * P.gamma + q * VEC, b);
       }
   } else {
     // processor I emits frame j (convolutional.py:319-327)
@@ -278,10 +298,8 @@ __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_c
   }
 }
 
-// per-slot fold of the emitted frame's bit count into (bit errors, frame errors)
-__global__ void fold_kernel(int32_t* cnt, int gamma, const int64_t* t_dev, long long t, int window) {
-  long long tt = t_dev ? (*t_dev + t) : t;
-  if (tt - window + 1 < 0) return;
+// fold the last emitted frame's bit count (end of a segment)
+__global__ void fold_kernel(int32_t* cnt, int gamma) {
   int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= gamma) return;
   int b = cnt[g];
@@ -304,37 +322,56 @@ CcParams make_params(const cc_plan* pl, int I, int gamma) {
   return P;
 }
 
-int pick_vec(int gamma) { return gamma >= 128 ? 4 : (gamma >= 64 ? 2 : 1); }
+// lanes per thread: check pass float2 (register-heavy), entry / variable float4
+inline int vec_for(int gamma, int want) {
+  if (want >= 4 && gamma % 128 == 0) return 4;
+  if (want >= 2 && gamma % 64 == 0) return 2;
+  return 1;
+}
 
-template <int VEC, bool QC>
+template <int DV, bool QC>
 void launch_entry(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
-  long long n = (long long)P.c * (P.gamma / VEC);
-  entry_kernel<VEC, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  int vec = vec_for(P.gamma, 4);
+  long long n = (long long)P.c * (P.gamma / vec);
+  unsigned nb = blocks_for(std::max<long long>(n, P.gamma));
+  if (vec == 4) entry_kernel<DV, 4, QC><<<nb, THREADS, 0, s>>>(a, P);
+  else if (vec == 2) entry_kernel<DV, 2, QC><<<nb, THREADS, 0, s>>>(a, P);
+  else entry_kernel<DV, 1, QC><<<nb, THREADS, 0, s>>>(a, P);
 }
-template <int DC, int VEC, bool QC>
+template <int DC, bool QC>
 void launch_check(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
-  long long n = (long long)P.I * P.cb * (P.gamma / VEC);
-  check_kernel<DC, VEC, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  int vec = vec_for(P.gamma, DC > 24 ? 1 : 2);
+  long long n = (long long)P.I * P.cb * (P.gamma / vec);
+  if (vec == 2) check_kernel<DC, 2, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  else check_kernel<DC, 1, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
 }
-template <int DV, int VEC, bool QC>
+template <int DV, bool QC>
 void launch_var(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
-  long long n = (long long)P.I * P.c * (P.gamma / VEC);
-  var_kernel<DV, VEC, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  int vec = vec_for(P.gamma, 4);
+  long long n = (long long)P.I * P.c * (P.gamma / vec);
+  if (vec == 4) var_kernel<DV, 4, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  else if (vec == 2) var_kernel<DV, 2, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  else var_kernel<DV, 1, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
 }
 
-template <int VEC, bool QC>
-int launch_slot_v(const CcParams& P, const SlotArgs& a, int dc, int dv, cudaStream_t s) {
-  launch_entry<VEC, QC>(P, a, s);
-  if (dc <= 8) launch_check<8, VEC, QC>(P, a, s);
-  else if (dc <= 16) launch_check<16, VEC, QC>(P, a, s);
-  else if (dc <= 24) launch_check<24, VEC, QC>(P, a, s);
-  else if (dc <= 32) launch_check<32, VEC, QC>(P, a, s);
+template <int DV, bool QC>
+int launch_slot_dv(const CcParams& P, const SlotArgs& a, int dc, cudaStream_t s) {
+  launch_entry<DV, QC>(P, a, s);
+  if (dc <= 8) launch_check<8, QC>(P, a, s);
+  else if (dc <= 16) launch_check<16, QC>(P, a, s);
+  else if (dc <= 24) launch_check<24, QC>(P, a, s);
+  else if (dc <= 32) launch_check<32, QC>(P, a, s);
   else return fail_arg("LDPCCC check degree > 32 is not supported");
-  if (dv <= 2) launch_var<2, VEC, QC>(P, a, s);
-  else if (dv <= 4) launch_var<4, VEC, QC>(P, a, s);
-  else if (dv <= 8) launch_var<8, VEC, QC>(P, a, s);
-  else return fail_arg("LDPCCC variable degree > 8 is not supported");
+  launch_var<DV, QC>(P, a, s);
   return 0;
+}
+
+template <bool QC>
+int launch_slot(const CcParams& P, const SlotArgs& a, int dc, int dv, cudaStream_t s) {
+  if (dv <= 2) return launch_slot_dv<2, QC>(P, a, dc, s);
+  if (dv <= 4) return launch_slot_dv<4, QC>(P, a, dc, s);
+  if (dv <= 8) return launch_slot_dv<8, QC>(P, a, dc, s);
+  return fail_arg("LDPCCC variable degree > 8 is not supported");
 }
 
 template <typename T>
@@ -439,21 +476,22 @@ int cc_slot(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev
   if (I < 1) return fail_arg("need at least one processor");
   if (gamma <= 0 || gamma % 32) return fail_arg("gamma must be a positive multiple of 32");
   if (!t_dev && t < 0) return fail_arg("slot index must be non-negative");
+  if (t > 0x3fffffff || t < -0x3fffffff) return fail_arg("slot index out of range");
   cudaStream_t s = as_stream(stream);
   CcParams P = make_params(pl, I, gamma);
-  SlotArgs a{msg, ring, mu_in, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (long long)t};
+  SlotArgs a{msg, ring, mu_in, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t};
   const bool qc = pl->all_live;
   const int dc = pl->lam * (qc ? pl->sl : pl->wmax);
   const int dv = pl->lam * pl->sj;
-  int rc;
-  switch (pick_vec(gamma)) {
-    case 4: rc = qc ? launch_slot_v<4, true>(P, a, dc, dv, s) : launch_slot_v<4, false>(P, a, dc, dv, s); break;
-    case 2: rc = qc ? launch_slot_v<2, true>(P, a, dc, dv, s) : launch_slot_v<2, false>(P, a, dc, dv, s); break;
-    default: rc = qc ? launch_slot_v<1, true>(P, a, dc, dv, s) : launch_slot_v<1, false>(P, a, dc, dv, s); break;
-  }
+  int rc = qc ? launch_slot<true>(P, a, dc, dv, s) : launch_slot<false>(P, a, dc, dv, s);
   if (rc) return rc;
-  if (lane_cnt) fold_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(lane_cnt, gamma, t_dev, t, I * pl->lam);
   return check_launch("cc_slot");
+}
+
+int cc_fold(int32_t* lane_cnt, int gamma, void* stream) {
+  if (!lane_cnt || gamma <= 0) return fail_arg("bad fold arguments");
+  fold_kernel<<<blocks_for(gamma), THREADS, 0, as_stream(stream)>>>(lane_cnt, gamma);
+  return check_launch("cc_fold");
 }
 
 int cc_advance(int64_t* t_dev, int64_t k, void* stream) {

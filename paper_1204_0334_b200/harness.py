@@ -252,9 +252,10 @@ class StreamCampaign:
                       self.gk, float(self.sigma), self.mu.data_ptr(), s)
             _lib.call("cc_slot", self.plan.handle, self.I, self.gk, t, None, self.msg.data_ptr(),
                       self.ring.data_ptr(), self.mu.data_ptr(), None, self.cnt.data_ptr(), s)
+        _lib.call("cc_fold", self.cnt.data_ptr(), self.gk, s)
 
     def kernel_launches_per_step(self) -> int:
-        return self.pushes * 5
+        return self.pushes * 4 + 1      # channel, entry(+fold), check, variable; final fold
 
     def step(self, lane0: int, sigma: float):
         import torch

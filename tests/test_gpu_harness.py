@@ -85,3 +85,31 @@ def test_bench_records(gpu):
     buf = io.StringIO()
     q.write_jsonl(recs, buf)
     assert [json.loads(l) for l in buf.getvalue().splitlines()] == recs
+
+
+def test_stream_campaign_unaligned_frames_vs_oracle(gpu):
+    """c = 18 (not a multiple of 4): frame starts t*c split Philox blocks."""
+    from oracle import campaign, qc as oqc
+    q = gpu
+    code = q.unwrap_qc(q.multiplicative_shifts(2, 4, 9))
+    assert code.c % 4 == 2
+    cfg = q.SimulationConfig("u", [2.5], processors=3, gamma=8, stop_block_errors=12,
+                             max_frames=400, seed=3, stream_segment_frames=7)
+    r = q.run_stream_simulation(code, cfg)[0]
+    U = oqc.unwrap(oqc.array_code_shifts(2, 4, 9), 9)
+    want = campaign.stream_point(U, 2.5, 0, processors=3, gamma=8, seed=3, stop=12, max_frames=400,
+                                 segment_frames=7)
+    assert (r.frames, r.bit_errors, r.frame_errors) == want
+
+
+def test_block_campaign_odd_n_vs_oracle(gpu):
+    from oracle import campaign, qc as oqc
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(3, 7, 11)))
+    assert lay.n_vars % 4 == 1
+    cfg = q.SimulationConfig("o", [2.0], iterations=10, gamma=16, stop_block_errors=20, max_frames=3000,
+                             seed=11)
+    r = q.run_block_simulation(lay, cfg)[0]
+    want = campaign.block_point(oqc.qc_layout(oqc.array_code_shifts(3, 7, 11), 11), 2.0, 0, iters=10,
+                                gamma=16, seed=11, stop=20, max_frames=3000)
+    assert (r.frames, r.bit_errors, r.frame_errors) == want

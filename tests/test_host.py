@@ -63,11 +63,13 @@ def test_qc_file_roundtrip(tmp_path, codes_npz):
         q.load_code(str(bad))
 
 
-def test_bundled_n18360_code_is_girth8():
-    h, exp = q.load_code(q.codes.bundled_code_path("n18360"))
-    assert (h.n, h.m, exp.edge_count) == (18360, 3060, 73440)
+@pytest.mark.parametrize("name,p,seed", [("n18360", 765, 18360), ("code_b_like", 632, 632),
+                                         ("code_c_like", 768, 768), ("code_d_like", 1024, 1024)])
+def test_bundled_codes_are_girth8_and_reproducible(name, p, seed):
+    h, exp = q.load_code(q.codes.bundled_code_path(name))
+    assert (h.n, h.m, exp.edge_count) == (24 * p, 4 * p, 96 * p)
     assert not codegen.has_short_cycles(exp.shifts, exp.p)
-    assert np.array_equal(codegen.girth8_shifts(4, 24, 765, seed=18360), exp.shifts)
+    assert np.array_equal(codegen.girth8_shifts(4, 24, p, seed=seed), exp.shifts)
 
 
 def test_lane_words_roundtrip():
