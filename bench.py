@@ -222,7 +222,7 @@ def main():
     from paper_1204_0334_b200.dist import init_from_env
 
     rank, W, group = init_from_env()
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     lay = code_n18360()
     N, M, E = lay.n_vars, lay.n_checks, lay.edge_count

@@ -22,18 +22,16 @@
 
 namespace qcb {
 
-// regular QC grid (every block live), staged into shared memory per CTA:
+// regular QC grid (every block live), a __grid_constant__ kernel parameter:
 // edge id of (block row j, circulant row r, block col l) = (j*p + r)*L + l,
 // its variable = l*p + (r + s_jl) mod p                      (codes.py:159-178)
+// gamma/VEC >= 32 for every launch, so all lanes of a warp belong to the same
+// check / variable and each shift lookup is a warp-uniform constant-bank load
+// (no shared-memory staging, no CTA barrier).
 struct QcGrid {
   int J, L, p;
   int16_t s[QC_MAX_J * QC_MAX_L];
 };
-
-__device__ __forceinline__ void stage_grid(const QcGrid& g, int16_t* sh) {
-  for (int i = threadIdx.x; i < g.J * g.L; i += blockDim.x) sh[i] = g.s[i];
-  __syncthreads();
-}
 
 enum CnuMode { CNU_BETA = 0, CNU_FROM_MU = 1, CNU_PHI = 2 };
 enum VnuMode { VNU_BETA = 0, VNU_PHI = 1, VNU_NONE = 2 };
@@ -106,8 +104,6 @@ __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned 
 // 188, and 3 forces spills -- both measured slower on B200.
 template <int DC, int VEC, bool REG, int MODE, bool QC>
 __global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid) {
-  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
-  if constexpr (QC && MODE == CNU_FROM_MU) stage_grid(grid, sh);
   if (a.done && *a.done) return;
   const int GV = a.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,7 +122,7 @@ __global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_co
         int v;
         if constexpr (QC) {
           int jrow = m / grid.p, r = m - jrow * grid.p;
-          int c = r + sh[jrow * grid.L + k];
+          int c = r + grid.s[jrow * grid.L + k];
           c -= (c >= grid.p) ? grid.p : 0;
           v = k * grid.p + c;
         } else {
@@ -147,8 +143,6 @@ __global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_co
 // one thread = (variable n, VEC consecutive lanes); d_v gathered packages
 template <int DV, int VEC, bool QC, int MODE>
 __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_constant__ QcGrid grid) {
-  __shared__ int16_t sh[QC_MAX_J * QC_MAX_L];
-  if constexpr (QC) stage_grid(grid, sh);
   if (a.done && *a.done) return;
   const int GV = a.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -162,7 +156,7 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
     int l = n / grid.p, c = n - l * grid.p;
 #pragma unroll
     for (int j = 0; j < DV; ++j) {
-      int rr = c - sh[j * grid.L + l];
+      int rr = c - grid.s[j * grid.L + l];
       rr += (rr < 0) ? grid.p : 0;
       e[j] = (j * grid.p + rr) * grid.L + l;
     }

@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "block_kernels.cuh"
 #include "phi.cuh"
 
 using namespace qcb;
@@ -81,17 +82,14 @@ __device__ __forceinline__ int pmod(int x, int m) {
   return r < 0 ? r + m : r;
 }
 
-__device__ __forceinline__ void stage(const CcParams& P, int16_t* sh) {
-  for (int i = threadIdx.x; i < P.J * P.L; i += blockDim.x) sh[i] = P.s[i];
-  __syncthreads();
-}
-
 // Edges of variable v (block column bc, circulant column cc) of a frame with
 // phase ph in group base `grp`, in the reference's summation order
 // (d = 0..T-1 over LUT_v[ph][d], then block row br; convolutional.py:414-423).
 // QC: local id of (br, bc) in sub-block (R, ph) = (br*p + (cc - s) mod p)*sl + bc.
+// Shift lookups are warp-uniform (gamma/VEC >= 32: a warp is one variable) and
+// read straight from the __grid_constant__ parameter bank.
 template <int DV, bool QC>
-__device__ __forceinline__ unsigned var_edges(const CcParams& P, const int16_t* sh, const int32_t* var_tab,
+__device__ __forceinline__ unsigned var_edges(const CcParams& P, const int32_t* var_tab,
                                               int ph, unsigned grp, int v, int bc, int cc, unsigned (&e)[DV]) {
   unsigned present = 0;
   const int T = P.lam;
@@ -105,7 +103,7 @@ __device__ __forceinline__ unsigned var_edges(const CcParams& P, const int16_t* 
       int lbl = R * T + ph;
       int loc;
       if constexpr (QC) {
-        int rr = cc - sh[(R * P.sj + br) * P.L + ph * P.sl + bc];
+        int rr = cc - P.s[(R * P.sj + br) * P.L + ph * P.sl + bc];
         rr += rr < 0 ? P.p : 0;
         loc = (br * P.p + rr) * P.sl + bc;
       } else {
@@ -158,8 +156,6 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
 // Also folds the previous slot's emitted-frame bit count into the lane counters.
 template <int DV, int VEC, bool QC>
 __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
-  __shared__ int16_t sh[CC_MAX_SHIFTS];
-  if constexpr (QC) stage(P, sh);
   const int t = slot_of(a);
   const int T = P.lam, GV = P.gamma / VEC, window = P.I * T;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -185,7 +181,7 @@ __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid
     m[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(m[i]))) | (__float_as_uint(m[i]) & 0x80000000u));
   const int bc = v / P.p, cc = v - bc * P.p;
   unsigned e[DV];
-  unsigned present = var_edges<DV, QC>(P, sh, a.var_tab, pmod(t, T), (unsigned)pmod(t / T, P.I) * (unsigned)P.E,
+  unsigned present = var_edges<DV, QC>(P, a.var_tab, pmod(t, T), (unsigned)pmod(t / T, P.I) * (unsigned)P.E,
                                         v, bc, cc, e);
 #pragma unroll
   for (int k = 0; k < DV; ++k)
@@ -237,7 +233,11 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
 #pragma unroll
   for (int k = 0; k < DC; ++k)
     if ((present >> k) & 1ull) vload<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
-  cnu_core_mask<DC, VEC>(x, present);
+  // steady state: every edge present -> the unmasked core of the block decoder
+  const int deg = T * W;
+  const unsigned long long full = deg >= 64 ? ~0ull : ((1ull << deg) - 1ull);
+  if (present == full) cnu_core<DC, VEC, true>(x, deg, (1u << VEC) - 1u);
+  else cnu_core_mask<DC, VEC>(x, present);
 #pragma unroll
   for (int k = 0; k < DC; ++k)
     if ((present >> k) & 1ull) vstore<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
@@ -246,8 +246,6 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
 // ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 ------
 template <int DV, int VEC, bool QC>
 __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
-  __shared__ int16_t sh[CC_MAX_SHIFTS];
-  if constexpr (QC) stage(P, sh);
   const int t = slot_of(a);
   const int T = P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -259,7 +257,7 @@ __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_c
   if (j < 0) return;
   const int bc = v / P.p, cc = v - bc * P.p;
   unsigned e[DV];
-  unsigned present = var_edges<DV, QC>(P, sh, a.var_tab, pmod(j, T), (unsigned)pmod(j / T, P.I) * (unsigned)P.E,
+  unsigned present = var_edges<DV, QC>(P, a.var_tab, pmod(j, T), (unsigned)pmod(j / T, P.I) * (unsigned)P.E,
                                         v, bc, cc, e);
   float tot[VEC], am[DV][VEC];
   vload<VEC>(a.ring + ((size_t)pmod(j, P.I * T) * P.c + v) * P.gamma + q * VEC, tot);

@@ -50,7 +50,9 @@ def main():
     print(json.dumps({"code": args.code, "I": args.I, "gamma": G, "pushes": pushes, "ms_per_segment": round(ms, 3),
                       "us_per_slot": round(ms * 1e3 / pushes, 2), "alg_gbs": round(gbs, 1),
                       "frac": round(gbs / peak, 4),
-                      "mbit_s": round(counted * G * (code.c - code.cb) / (ms / 1e3) / 1e6, 1)}), flush=True)
+                      "mbit_s": round(counted * G * (code.c - code.cb) / (ms / 1e3) / 1e6, 1),
+                      # a frame is decoded I*T slots after it is pushed
+                      "latency_ms": round(window * ms / pushes, 3)}), flush=True)
 
 
 if __name__ == "__main__":
