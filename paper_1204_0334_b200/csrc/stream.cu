@@ -88,11 +88,29 @@ __device__ __forceinline__ int pmod(int x, int m) {
 // QC: local id of (br, bc) in sub-block (R, ph) = (br*p + (cc - s) mod p)*sl + bc.
 // Shift lookups are warp-uniform (gamma/VEC >= 32: a warp is one variable) and
 // read straight from the __grid_constant__ parameter bank.
-template <int DV, bool QC>
+template <int DV, bool QC, int TT = 0, int SJ = 0>
 __device__ __forceinline__ unsigned var_edges(const CcParams& P, const int32_t* var_tab,
                                               int ph, unsigned grp, int v, int bc, int cc, unsigned (&e)[DV]) {
   unsigned present = 0;
-  const int T = P.lam;
+  const int T = TT ? TT : P.lam;
+  if constexpr (QC && TT > 0 && SJ > 0) {
+    static_assert(TT * SJ <= DV, "bucket too small");
+#pragma unroll
+    for (int d = 0; d < TT; ++d) {
+      int R = ph + d;
+      R -= (R >= TT) ? TT : 0;
+      const int lbl = R * TT + ph;
+#pragma unroll
+      for (int br = 0; br < SJ; ++br) {
+        int rr = cc - P.s[(R * SJ + br) * P.L + ph * P.sl + bc];
+        rr += rr < 0 ? P.p : 0;
+        e[d * SJ + br] = grp + (unsigned)P.sub_off[lbl] + (unsigned)((br * P.p + rr) * P.sl + bc);
+      }
+    }
+#pragma unroll
+    for (int k = TT * SJ; k < DV; ++k) e[k] = 0;
+    return (1u << (TT * SJ)) - 1u;
+  }
   int d = 0, br = 0;
 #pragma unroll
   for (int k = 0; k < DV; ++k) {
@@ -154,10 +172,10 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
 
 // ---- entry: frame t into ring slot t mod window and its T sub-blocks --------
 // Also folds the previous slot's emitted-frame bit count into the lane counters.
-template <int DV, int VEC, bool QC>
+template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
 __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   const int t = slot_of(a);
-  const int T = P.lam, GV = P.gamma / VEC, window = P.I * T;
+  const int T = TT ? TT : P.lam, GV = P.gamma / VEC, window = P.I * T;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (a.cnt && t >= window && tid < P.gamma) {   // previous slot emitted a frame
     int g = (int)tid;
@@ -181,18 +199,20 @@ __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid
     m[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(m[i]))) | (__float_as_uint(m[i]) & 0x80000000u));
   const int bc = v / P.p, cc = v - bc * P.p;
   unsigned e[DV];
-  unsigned present = var_edges<DV, QC>(P, a.var_tab, pmod(t, T), (unsigned)pmod(t / T, P.I) * (unsigned)P.E,
-                                        v, bc, cc, e);
+  unsigned present = var_edges<DV, QC, TT, SJ>(P, a.var_tab, pmod(t, T), (unsigned)pmod(t / T, P.I) * (unsigned)P.E,
+                                                v, bc, cc, e);
 #pragma unroll
   for (int k = 0; k < DV; ++k)
     if ((present >> k) & 1u) vstore<VEC>(a.msg + (size_t)e[k] * P.gamma + q * VEC, m);
 }
 
 // ---- check phase: processors i = 1..I refresh layer s = t - (i-1)T ---------
-template <int DC, int VEC, bool QC>
+// TT, WW > 0: period and sub-block width known at compile time (QC grids of the
+// common shapes) so the edge walk fully unrolls; 0 = runtime values.
+template <int DC, int VEC, bool QC, int TT = 0, int WW = 0>
 __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   const int t = slot_of(a);
-  const int T = P.lam, GV = P.gamma / VEC;
+  const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)P.I * P.cb * GV) return;
   int ip = (int)(tid / ((long long)P.cb * GV));
@@ -201,9 +221,30 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
   const int s = t - ip * T;
   if (s < 0) return;
   const int kap = pmod(s, T);
-  const int W = QC ? P.sl : P.wmax;
+  const int W = WW ? WW : (QC ? P.sl : P.wmax);
   unsigned eidx[DC];   // package index (I*E < 2^32)
   unsigned long long present = 0;
+  if constexpr (TT > 0 && WW > 0 && QC) {
+    // compile-time walk: d = k / WW, w = k % WW
+    static_assert(TT * WW <= DC, "bucket too small");
+#pragma unroll
+    for (int d = 0; d < TT; ++d) {
+      const int f = s - (TT - 1) + d;
+      int c2 = kap + 1 + d;
+      c2 -= (c2 >= TT) ? TT : 0;
+      c2 -= (c2 >= TT) ? TT : 0;
+      const int lbl = kap * TT + c2;
+      const unsigned base = f >= 0 ? (unsigned)pmod(f / TT, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] +
+                                         (unsigned)(r * WW) : 0u;
+#pragma unroll
+      for (int w = 0; w < WW; ++w) {
+        eidx[d * WW + w] = base + w;
+        if (f >= 0) present |= 1ull << (d * WW + w);
+      }
+    }
+#pragma unroll
+    for (int k = TT * WW; k < DC; ++k) eidx[k] = 0;
+  } else {
   // walk d = 0..T-1 (frames s-ms+d, oldest first) and w = 0..W-1 incrementally
   int d = 0, w = 0;
   int f = s - P.ms;
@@ -229,6 +270,7 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
       }
     }
   }
+  }
   float x[DC][VEC];
 #pragma unroll
   for (int k = 0; k < DC; ++k)
@@ -244,10 +286,10 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
 }
 
 // ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 ------
-template <int DV, int VEC, bool QC>
+template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
 __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   const int t = slot_of(a);
-  const int T = P.lam, GV = P.gamma / VEC;
+  const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)P.I * P.c * GV) return;
   int ip = (int)(tid / ((long long)P.c * GV));
@@ -257,8 +299,8 @@ __global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_c
   if (j < 0) return;
   const int bc = v / P.p, cc = v - bc * P.p;
   unsigned e[DV];
-  unsigned present = var_edges<DV, QC>(P, a.var_tab, pmod(j, T), (unsigned)pmod(j / T, P.I) * (unsigned)P.E,
-                                        v, bc, cc, e);
+  unsigned present = var_edges<DV, QC, TT, SJ>(P, a.var_tab, pmod(j, T), (unsigned)pmod(j / T, P.I) * (unsigned)P.E,
+                                                v, bc, cc, e);
   float tot[VEC], am[DV][VEC];
   vload<VEC>(a.ring + ((size_t)pmod(j, P.I * T) * P.c + v) * P.gamma + q * VEC, tot);
 #pragma unroll
@@ -327,35 +369,52 @@ inline int vec_for(int gamma, int want) {
   return 1;
 }
 
-template <int DV, bool QC>
+template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_entry(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
   long long n = (long long)P.c * (P.gamma / vec);
   unsigned nb = blocks_for(std::max<long long>(n, P.gamma));
-  if (vec == 4) entry_kernel<DV, 4, QC><<<nb, THREADS, 0, s>>>(a, P);
-  else if (vec == 2) entry_kernel<DV, 2, QC><<<nb, THREADS, 0, s>>>(a, P);
-  else entry_kernel<DV, 1, QC><<<nb, THREADS, 0, s>>>(a, P);
+  if (vec == 4) entry_kernel<DV, 4, QC, TT, SJ><<<nb, THREADS, 0, s>>>(a, P);
+  else if (vec == 2) entry_kernel<DV, 2, QC, TT, SJ><<<nb, THREADS, 0, s>>>(a, P);
+  else entry_kernel<DV, 1, QC, TT, SJ><<<nb, THREADS, 0, s>>>(a, P);
 }
-template <int DC, bool QC>
+template <int DC, bool QC, int TT = 0, int WW = 0>
 void launch_check(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, DC > 24 ? 1 : 2);
   long long n = (long long)P.I * P.cb * (P.gamma / vec);
-  if (vec == 2) check_kernel<DC, 2, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
-  else check_kernel<DC, 1, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  if (vec == 2) check_kernel<DC, 2, QC, TT, WW><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  else check_kernel<DC, 1, QC, TT, WW><<<blocks_for(n), THREADS, 0, s>>>(a, P);
 }
-template <int DV, bool QC>
+template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_var(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
   long long n = (long long)P.I * P.c * (P.gamma / vec);
-  if (vec == 4) var_kernel<DV, 4, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
-  else if (vec == 2) var_kernel<DV, 2, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
-  else var_kernel<DV, 1, QC><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  if (vec == 4) var_kernel<DV, 4, QC, TT, SJ><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  else if (vec == 2) var_kernel<DV, 2, QC, TT, SJ><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  else var_kernel<DV, 1, QC, TT, SJ><<<blocks_for(n), THREADS, 0, s>>>(a, P);
 }
 
 template <int DV, bool QC>
 int launch_slot_dv(const CcParams& P, const SlotArgs& a, int dc, cudaStream_t s) {
+  if constexpr (QC && DV == 4) {   // compile-time walks for the common unwrapped shapes
+    if (P.lam == 4 && P.sj == 1 && P.sl == 6) {          // (4, 24) grids: codes A', 18360'
+      launch_entry<4, true, 4, 1>(P, a, s); launch_check<24, true, 4, 6>(P, a, s); launch_var<4, true, 4, 1>(P, a, s);
+      return 0;
+    }
+    if (P.lam == 4 && P.sj == 1 && P.sl == 2) {          // (4, 8) grids
+      launch_entry<4, true, 4, 1>(P, a, s); launch_check<8, true, 4, 2>(P, a, s); launch_var<4, true, 4, 1>(P, a, s);
+      return 0;
+    }
+  }
+  if constexpr (QC && DV == 2) {
+    if (P.lam == 2 && P.sj == 1 && P.sl == 2) {          // (2, 4) grids
+      launch_entry<2, true, 2, 1>(P, a, s); launch_check<4, true, 2, 2>(P, a, s); launch_var<2, true, 2, 1>(P, a, s);
+      return 0;
+    }
+  }
   launch_entry<DV, QC>(P, a, s);
-  if (dc <= 8) launch_check<8, QC>(P, a, s);
+  if (dc <= 4) launch_check<4, QC>(P, a, s);
+  else if (dc <= 8) launch_check<8, QC>(P, a, s);
   else if (dc <= 16) launch_check<16, QC>(P, a, s);
   else if (dc <= 24) launch_check<24, QC>(P, a, s);
   else if (dc <= 32) launch_check<32, QC>(P, a, s);
