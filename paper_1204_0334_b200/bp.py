@@ -245,10 +245,10 @@ class BlockDecoder:
         _lib.call("qc_llr_from_lane_major", n, self.gp, gi, self._x.data_ptr(),
                   float(sigma) if sigma is not None else 0.0, self.mu.data_ptr(), _stream())
 
-    def result(self, gamma: int) -> DecodeResult:
-        """Lane-major results on the host: posteriors leave the GPU as fp32 (the
-        precision they were computed in) and are widened to float64 on the host
-        by a multi-threaded copy; hard bits, syndrome flags, iteration counts."""
+    def stage_result(self, gamma: int):
+        """Queue the lane-major conversion and the device->host copies of the
+        first `gamma` lanes (posteriors as fp32, the precision they were
+        computed in; hard bits; syndrome flags; iteration counts)."""
         import torch
         n = self.layout.n_vars
         if getattr(self, "_lm", None) is None or self._lm[0].shape[0] != gamma:
@@ -264,20 +264,79 @@ class BlockDecoder:
         hb.copy_(bits_d, non_blocking=True)
         hs[0].copy_(self.ok.to(torch.int32), non_blocking=True)
         hs[1].copy_(self.iters, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        post = torch.empty((gamma, n), dtype=torch.float64)
-        post.copy_(hp)
-        bits = torch.empty((gamma, n), dtype=torch.uint8)
-        bits.copy_(hb)
-        small = hs.numpy()
-        return DecodeResult(hard_bits=bits.numpy(), posteriors=post.numpy(),
-                            syndrome_ok=small[0, :gamma].astype(bool),
-                            iterations_run=small[1, :gamma].astype(np.int64))
+        self._done = torch.cuda.Event()
+        self._done.record()
+
+    def collect_result(self, gamma: int, post, bits, ok, its, at: int = 0):
+        """Wait for stage_result and write lanes into host arrays at row `at`
+        (multi-threaded copies; fp32 posteriors widen to float64)."""
+        import torch
+        self._done.synchronize()
+        torch.from_numpy(post[at:at + gamma]).copy_(self._host["post"])
+        torch.from_numpy(bits[at:at + gamma]).copy_(self._host["bits"])
+        small = self._host["small"].numpy()
+        ok[at:at + gamma] = small[0, :gamma].astype(bool)
+        its[at:at + gamma] = small[1, :gamma]
+
+    def result(self, gamma: int) -> DecodeResult:
+        n = self.layout.n_vars
+        post = np.empty((gamma, n), dtype=np.float64)
+        bits = np.empty((gamma, n), dtype=np.uint8)
+        ok = np.empty(gamma, dtype=bool)
+        its = np.empty(gamma, dtype=np.int64)
+        self.stage_result(gamma)
+        self.collect_result(gamma, post, bits, ok, its)
+        return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
 
 
-def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool) -> BlockDecoder:
+PIPELINE_CHUNK = 1024   # lanes per pipelined chunk of the host-buffer API
+
+
+def _pipelined(layout: EdgeLayout, x: np.ndarray, sigma, iterations: int, early_stop: bool) -> DecodeResult:
+    """Host-buffer decode of a large batch in chunks of PIPELINE_CHUNK lanes on
+    two CUDA streams: while chunk k decodes, chunk k+1 is copied in and chunk
+    k-1 is read back, so the PCIe / host-memory traffic overlaps the kernels."""
+    import torch
+    G, n = x.shape
+    post = np.empty((G, n), dtype=np.float64)
+    bits = np.empty((G, n), dtype=np.uint8)
+    ok = np.empty(G, dtype=bool)
+    its = np.empty(G, dtype=np.int64)
+    decs = [_decoder(layout, PIPELINE_CHUNK, iterations, early_stop, slot=i) for i in (0, 1)]
+    cache = layout.__dict__.setdefault("_streams", [])
+    while len(cache) < 2:
+        cache.append(torch.cuda.Stream())
+    streams = cache[:2]
+    cur = torch.cuda.current_stream()
+    for st in streams:
+        st.wait_stream(cur)
+    pending = [None, None]
+    starts = list(range(0, G, PIPELINE_CHUNK))
+    for k, a in enumerate(starts):
+        b = min(G, a + PIPELINE_CHUNK)
+        i = k % 2
+        if pending[i] is not None:
+            pa, pb = pending[i]
+            decs[i].collect_result(pb - pa, post, bits, ok, its, pa)
+        with torch.cuda.stream(streams[i]):
+            decs[i].load_lane_major(x[a:b], sigma)
+            decs[i].run()
+            decs[i].stage_result(b - a)
+        pending[i] = (a, b)
+    for k in range(len(starts), len(starts) + 2):
+        i = k % 2
+        if pending[i] is not None:
+            pa, pb = pending[i]
+            decs[i].collect_result(pb - pa, post, bits, ok, its, pa)
+            pending[i] = None
+    for st in streams:
+        cur.wait_stream(st)
+    return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
+
+
+def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool, slot: int = 0) -> BlockDecoder:
     cache = layout.__dict__.setdefault("_decoders", {})
-    key = (pad32(gamma), iterations, bool(early_stop))
+    key = (pad32(gamma), iterations, bool(early_stop), slot)
     dec = cache.get(key)
     if dec is None:
         if len(cache) >= 8:
@@ -295,6 +354,8 @@ def decode_llr_batch(layout: EdgeLayout, mu: np.ndarray, iterations: int,
     mu = np.atleast_2d(np.asarray(mu, dtype=np.float64))
     if mu.shape[1] != layout.n_vars:
         raise ValueError(f"mu has {mu.shape[1]} symbols, layout has {layout.n_vars}")
+    if mu.shape[0] > 2 * PIPELINE_CHUNK:
+        return _pipelined(layout, mu, None, iterations, early_stop)
     dec = _decoder(layout, mu.shape[0], iterations, early_stop)
     dec.load_lane_major(mu, None)
     dec.run()
@@ -309,8 +370,11 @@ def decode_batch(layout: EdgeLayout, y: np.ndarray, sigma: float, iterations: in
         raise ValueError(f"y has {y.shape[1]} symbols, layout has {layout.n_vars}")
     if iterations < 1:
         raise ValueError("need at least one iteration")
-    dec = _decoder(layout, y.shape[0], iterations, early_stop)
     s = abs(float(sigma))
-    dec.load_lane_major(y, s if s > 0.0 else 1e-300)
+    s = s if s > 0.0 else 1e-300
+    if y.shape[0] > 2 * PIPELINE_CHUNK:
+        return _pipelined(layout, y, s, iterations, early_stop)
+    dec = _decoder(layout, y.shape[0], iterations, early_stop)
+    dec.load_lane_major(y, s)
     dec.run()
     return dec.result(y.shape[0])

@@ -201,3 +201,21 @@ def test_decode_errors(gpu):
     r1 = q.decode_batch(lay, np.random.default_rng(2).normal(1, .8, (3, lay.n_vars)), 0.8, 6)
     r2 = q.decode_llr_batch(lay, q.channel_llrs(np.random.default_rng(2).normal(1, .8, (3, lay.n_vars)), 0.8), 6)
     assert np.array_equal(r1.posteriors, r2.posteriors)
+
+
+def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
+    """decode_batch above 2 x PIPELINE_CHUNK lanes runs chunked on two streams."""
+    q = gpu
+    from paper_1204_0334_b200 import bp as qbp
+    monkeypatch.setattr(qbp, "PIPELINE_CHUNK", 64)
+    lay = toy(q)
+    rng = np.random.default_rng(77)
+    y = rng.normal(1.0, 1.0, size=(300, lay.n_vars))
+    r = q.decode_batch(lay, y, 1.0, 12)
+    olay = oqc.qc_layout(oqc.array_code_shifts(2, 4, 8), 8)
+    bits, post, ok, its = obp.decode_llr(olay, obp.channel_llrs(y, 1.0), 12)
+    assert np.array_equal(r.hard_bits, bits) and np.array_equal(r.syndrome_ok, ok)
+    assert np.array_equal(r.iterations_run, its)
+    close(r.posteriors, post)
+    r2 = q.decode_batch(lay, y[:64], 1.0, 12)
+    assert np.array_equal(r2.posteriors, r.posteriors[:64])
