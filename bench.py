@@ -40,6 +40,21 @@ ITERS = 30
 EBN0 = 3.2
 
 
+def ncu_traffic(kernel_tag: str, gamma: int):
+    """DRAM bytes (read + write) per launch of the dominant kernel from a committed
+    ncu capture (profiles/*/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(REPO, "profiles", "*", "ncu_traffic.json"))):
+        try:
+            for rec in json.load(open(p)):
+                if rec.get("tag") == kernel_tag and int(rec.get("gamma", -1)) == gamma:
+                    best = rec
+        except Exception:
+            pass
+    return best
+
+
 def load_peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -287,8 +302,11 @@ def main():
     peak, peak_kind = load_peaks()
     achieved = cnu_bytes / (cnu_ms / 1e3) / 1e9
     step_alg = algorithmic_bytes_per_codeword(E, N, ITERS) * gamma
+    tr = ncu_traffic("cnu_phi", gamma)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4),
+                "traffic": int(tr["dram_bytes"]) if tr else None,
+                "traffic_source": tr["source"] if tr else None,
                 "kernel": "cnu_kernel<24,VEC,REG,CNU_PHI> (check-node pass, phi form)", "peak_kind": peak_kind,
                 "bytes_per_launch": cnu_bytes, "launch_ms": round(cnu_ms, 4),
                 "vnu": {"achieved": round(vnu_bytes / (vnu_ms / 1e3) / 1e9, 1), "launch_ms": round(vnu_ms, 4),

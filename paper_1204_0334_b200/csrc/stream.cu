@@ -221,68 +221,83 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
   const int s = t - ip * T;
   if (s < 0) return;
   const int kap = pmod(s, T);
-  const int W = WW ? WW : (QC ? P.sl : P.wmax);
-  unsigned eidx[DC];   // package index (I*E < 2^32)
-  unsigned long long present = 0;
+  float x[DC][VEC];
   if constexpr (TT > 0 && WW > 0 && QC) {
-    // compile-time walk: d = k / WW, w = k % WW
+    // compile-time walk: edge k = d*WW + w sits at package base[d] + w, so
+    // only TT base addresses stay live (registers -> occupancy)
     static_assert(TT * WW <= DC, "bucket too small");
+    unsigned base[TT];
+    unsigned present = 0;   // one bit per frame d
 #pragma unroll
     for (int d = 0; d < TT; ++d) {
       const int f = s - (TT - 1) + d;
       int c2 = kap + 1 + d;
       c2 -= (c2 >= TT) ? TT : 0;
       c2 -= (c2 >= TT) ? TT : 0;
-      const int lbl = kap * TT + c2;
-      const unsigned base = f >= 0 ? (unsigned)pmod(f / TT, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] +
-                                         (unsigned)(r * WW) : 0u;
-#pragma unroll
-      for (int w = 0; w < WW; ++w) {
-        eidx[d * WW + w] = base + w;
-        if (f >= 0) present |= 1ull << (d * WW + w);
-      }
+      base[d] = f >= 0 ? (unsigned)pmod(f / TT, P.I) * (unsigned)P.E + (unsigned)P.sub_off[kap * TT + c2] +
+                             (unsigned)(r * WW) : 0u;
+      present |= (f >= 0 ? 1u : 0u) << d;   // bootstrap: absent frames drop out (convolutional.py:276-279)
     }
 #pragma unroll
-    for (int k = TT * WW; k < DC; ++k) eidx[k] = 0;
+    for (int d = 0; d < TT; ++d)
+#pragma unroll
+      for (int w = 0; w < WW; ++w)
+        if ((present >> d) & 1u) vload<VEC>(a.msg + (size_t)(base[d] + w) * P.gamma + q * VEC, x[d * WW + w]);
+    if (present == (1u << TT) - 1u) {
+      cnu_core<DC, VEC, true>(x, TT * WW, (1u << VEC) - 1u);   // steady state
+    } else {
+      unsigned long long pm = 0;
+#pragma unroll
+      for (int d = 0; d < TT; ++d)
+        if ((present >> d) & 1u) pm |= ((1ull << WW) - 1ull) << (d * WW);
+      cnu_core_mask<DC, VEC>(x, pm);
+    }
+#pragma unroll
+    for (int d = 0; d < TT; ++d)
+#pragma unroll
+      for (int w = 0; w < WW; ++w)
+        if ((present >> d) & 1u) vstore<VEC>(a.msg + (size_t)(base[d] + w) * P.gamma + q * VEC, x[d * WW + w]);
+    return;
   } else {
-  // walk d = 0..T-1 (frames s-ms+d, oldest first) and w = 0..W-1 incrementally
-  int d = 0, w = 0;
-  int f = s - P.ms;
-  int lbl = kap * T + (kap + 1 < T ? kap + 1 : kap + 1 - T);
-  unsigned base = f >= 0 ? (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] : 0u;
+    const int W = QC ? P.sl : P.wmax;
+    unsigned eidx[DC];   // package index (I*E < 2^32)
+    unsigned long long present = 0;
+    // walk d = 0..T-1 (frames s-ms+d, oldest first) and w = 0..W-1 incrementally
+    int d = 0, w = 0;
+    int f = s - P.ms;
+    int lbl = kap * T + (kap + 1 < T ? kap + 1 : kap + 1 - T);
+    unsigned base = f >= 0 ? (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] : 0u;
 #pragma unroll
-  for (int k = 0; k < DC; ++k) {
-    eidx[k] = 0;
-    if (k < T * W) {
-      if (f >= 0) {   // bootstrap: absent frames drop out (convolutional.py:276-279)
-        int loc;
-        if constexpr (QC) loc = r * P.sl + w;
-        else loc = a.check_tab[((size_t)lbl * P.cb + r) * P.wmax + w];
-        if (loc >= 0) { eidx[k] = base + (unsigned)loc; present |= 1ull << k; }
-      }
-      if (++w == W) {
-        w = 0; ++d; ++f;
-        int c2 = kap + 1 + d;
-        c2 -= (c2 >= T) ? T : 0;
-        c2 -= (c2 >= T) ? T : 0;
-        lbl = kap * T + c2;
-        base = f >= 0 ? (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] : 0u;
+    for (int k = 0; k < DC; ++k) {
+      eidx[k] = 0;
+      if (k < T * W) {
+        if (f >= 0) {
+          int loc;
+          if constexpr (QC) loc = r * P.sl + w;
+          else loc = a.check_tab[((size_t)lbl * P.cb + r) * P.wmax + w];
+          if (loc >= 0) { eidx[k] = base + (unsigned)loc; present |= 1ull << k; }
+        }
+        if (++w == W) {
+          w = 0; ++d; ++f;
+          int c2 = kap + 1 + d;
+          c2 -= (c2 >= T) ? T : 0;
+          c2 -= (c2 >= T) ? T : 0;
+          lbl = kap * T + c2;
+          base = f >= 0 ? (unsigned)pmod(f / T, P.I) * (unsigned)P.E + (unsigned)P.sub_off[lbl] : 0u;
+        }
       }
     }
-  }
-  }
-  float x[DC][VEC];
 #pragma unroll
-  for (int k = 0; k < DC; ++k)
-    if ((present >> k) & 1ull) vload<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
-  // steady state: every edge present -> the unmasked core of the block decoder
-  const int deg = T * W;
-  const unsigned long long full = deg >= 64 ? ~0ull : ((1ull << deg) - 1ull);
-  if (present == full) cnu_core<DC, VEC, true>(x, deg, (1u << VEC) - 1u);
-  else cnu_core_mask<DC, VEC>(x, present);
+    for (int k = 0; k < DC; ++k)
+      if ((present >> k) & 1ull) vload<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
+    const int deg = T * W;
+    const unsigned long long full = deg >= 64 ? ~0ull : ((1ull << deg) - 1ull);
+    if (present == full) cnu_core<DC, VEC, true>(x, deg, (1u << VEC) - 1u);
+    else cnu_core_mask<DC, VEC>(x, present);
 #pragma unroll
-  for (int k = 0; k < DC; ++k)
-    if ((present >> k) & 1ull) vstore<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
+    for (int k = 0; k < DC; ++k)
+      if ((present >> k) & 1ull) vstore<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
+  }
 }
 
 // ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 ------
