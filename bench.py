@@ -219,7 +219,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--gamma", type=int, default=4096)
-    ap.add_argument("--stream-gamma", type=int, default=256, help="lanes of the LDPCCC measurement (0 = skip)")
+    ap.add_argument("--stream-gamma", type=int, default=512, help="lanes of the LDPCCC measurement (0 = skip)")
     ap.add_argument("--stream-steps", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-batches", type=int, default=0, help="cpu_baseline sample size (0 = cores)")
