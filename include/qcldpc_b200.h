@@ -110,6 +110,24 @@ QC_API int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post,
 QC_API int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma,
                                   float* mu_vm, void* stream);
 
+/* ---- float64 conformance build (block decoder) ---------------------------
+ * The reference's own arithmetic (tanh rule with sequential forward/backward
+ * products, bp.py:120-188) in float64 on the GPU, for callers relying on the
+ * reference's 1e-12 tolerances.  Same layouts with double packages. */
+QC_API int qc64_init(const qc_plan* plan, int gamma, const double* mu, double* msgs, void* stream);
+QC_API int qc64_cnu(const qc_plan* plan, int gamma, double* msgs, const uint32_t* active, void* stream);
+QC_API int qc64_vnu(const qc_plan* plan, int gamma, double* msgs, const double* mu, double* post,
+                    uint32_t* hb, const uint32_t* active, void* stream);
+QC_API int qc64_hard_bits(const qc_plan* plan, int gamma, const double* post, uint32_t* hb, void* stream);
+QC_API int qc64_decode(const qc_plan* plan, int gamma, int iters, int early_stop, const double* mu,
+                       double* msgs, double* post, uint32_t* hb, uint32_t* work, uint8_t* ok,
+                       int32_t* iters_run, void* stream);
+QC_API int qc64_lane_major(int n, int gamma, int gamma_out, const double* post, double* post_out,
+                           uint8_t* bits_out, void* stream);
+/* lane-major fp64 -> variable-major fp64 mu; sigma > 0: (2x)/(sigma sigma); clip: saturate +-50 */
+QC_API int qc64_mu_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma,
+                                   int clip, double* mu, void* stream);
+
 /* ---- channel (channel.py:61-105) ---------------------------------------- */
 /* y[g, k] = 1 + sigma * ndtri(u(philox word at position start+k of lane lane0+g)),
  * mu = clip(2y/sigma^2, +-50) (bp.py:54-56).  Outputs (any may be NULL):

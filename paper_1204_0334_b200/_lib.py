@@ -42,6 +42,13 @@ SIGNATURES = {
     "qc_lane_major": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_lane_major_f32": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_llr_from_lane_major": (_i, [_i, _i, _i, _p, _d, _p, _p]),
+    "qc64_init": (_i, [_p, _i, _p, _p, _p]),
+    "qc64_cnu": (_i, [_p, _i, _p, _p, _p]),
+    "qc64_vnu": (_i, [_p, _i, _p, _p, _p, _p, _p, _p]),
+    "qc64_hard_bits": (_i, [_p, _i, _p, _p, _p]),
+    "qc64_decode": (_i, [_p, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "qc64_lane_major": (_i, [_i, _i, _i, _p, _p, _p, _p]),
+    "qc64_mu_from_lane_major": (_i, [_i, _i, _i, _p, _d, _i, _p, _p]),
     "qc_channel": (_i, [_u64, _u64, _u64, _u64, _i, _i, _d, _p, _p, _p, _p]),
     "qc_channel_dev": (_i, [_u64, _u64, _p, _u64, _i, _i, _d, _p, _p]),
     "qc_lane_advance": (_i, [_p, _u64, _p]),

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _lib
 from .codes import EdgeLayout
-from .plan import lane_words, pad32, require_cuda, unpack_planes
+from .plan import get_precision, lane_words, pad32, require_cuda, unpack_planes
 
 __all__ = [
     "L_MAX", "TANH_CLAMP", "MessageBatch", "DecodeResult", "channel_llrs", "init_messages",
@@ -61,14 +61,16 @@ class MessageBatch:
         self.gamma = mu.shape[1]
         self.mu = mu
         self._gp = pad32(self.gamma)
+        self.fp64 = get_precision() == "float64"
+        dt = torch.float64 if self.fp64 else torch.float32
         dev = torch.device("cuda", torch.cuda.current_device())
-        m = torch.full((layout.n_vars, self._gp), L_MAX, dtype=torch.float32)
-        m[:, : self.gamma] = torch.from_numpy(mu).float()
+        m = torch.full((layout.n_vars, self._gp), L_MAX, dtype=dt)
+        m[:, : self.gamma] = torch.from_numpy(mu).to(dt)
         self._mu_dev = m.to(dev)
-        self._msgs = torch.zeros((max(layout.edge_count, 1), self._gp), dtype=torch.float32, device=dev)
+        self._msgs = torch.zeros((max(layout.edge_count, 1), self._gp), dtype=dt, device=dev)
         if layout.edge_count:
-            _lib.call("qc_init", layout.plan().handle, self._gp, self._mu_dev.data_ptr(),
-                      self._msgs.data_ptr(), _stream())
+            _lib.call("qc64_init" if self.fp64 else "qc_init", layout.plan().handle, self._gp,
+                      self._mu_dev.data_ptr(), self._msgs.data_ptr(), _stream())
 
     @property
     def packages_device(self):
@@ -109,8 +111,8 @@ def check_node_update(batch: MessageBatch, layout: EdgeLayout, active: np.ndarra
     if layout.edge_count == 0:
         return
     act = _active_dev(active, batch._gp)
-    _lib.call("qc_cnu", layout.plan().handle, batch._gp, batch._msgs.data_ptr(),
-              _lib.ptr(act), _stream())
+    _lib.call("qc64_cnu" if batch.fp64 else "qc_cnu", layout.plan().handle, batch._gp,
+              batch._msgs.data_ptr(), _lib.ptr(act), _stream())
 
 
 def variable_node_update(batch: MessageBatch, layout: EdgeLayout,
@@ -118,9 +120,10 @@ def variable_node_update(batch: MessageBatch, layout: EdgeLayout,
     """Packages <- variable-to-check messages; returns posteriors (N, gamma) (bp.py:165-188)."""
     import torch
     act = _active_dev(active, batch._gp)
-    post = torch.zeros((layout.n_vars, batch._gp), dtype=torch.float32, device=batch._msgs.device)
-    _lib.call("qc_vnu", layout.plan().handle, batch._gp, batch._msgs.data_ptr(),
-              batch._mu_dev.data_ptr(), post.data_ptr(), None, _lib.ptr(act), _stream())
+    post = torch.zeros((layout.n_vars, batch._gp), dtype=batch._msgs.dtype, device=batch._msgs.device)
+    _lib.call("qc64_vnu" if batch.fp64 else "qc_vnu", layout.plan().handle, batch._gp,
+              batch._msgs.data_ptr(), batch._mu_dev.data_ptr(), post.data_ptr(), None,
+              _lib.ptr(act), _stream())
     return post[:, : batch.gamma].double().cpu().numpy()
 
 
@@ -130,15 +133,21 @@ def hard_decision_and_syndrome(layout: EdgeLayout, posteriors: np.ndarray):
     post = np.asarray(posteriors, dtype=np.float64)
     n, g = post.shape
     gp = pad32(g)
-    p32 = post.astype(np.float32)
-    p32[(post < 0) & (p32 == 0)] = -1.0        # keep the sign of tiny negatives
-    dev = torch.zeros((n, gp), dtype=torch.float32)
-    dev[:, :g] = torch.from_numpy(p32)
+    fp64 = get_precision() == "float64"
+    if fp64:
+        dev = torch.zeros((n, gp), dtype=torch.float64)
+        dev[:, :g] = torch.from_numpy(post)
+    else:
+        p32 = post.astype(np.float32)
+        p32[(post < 0) & (p32 == 0)] = -1.0        # keep the sign of tiny negatives
+        dev = torch.zeros((n, gp), dtype=torch.float32)
+        dev[:, :g] = torch.from_numpy(p32)
     dev = dev.cuda()
     hb = torch.zeros((n, gp // 32), dtype=torch.int32, device=dev.device)
     bad = torch.zeros(gp // 32, dtype=torch.int32, device=dev.device)
     plan = layout.plan()
-    _lib.call("qc_hard_bits", plan.handle, gp, dev.data_ptr(), hb.data_ptr(), _stream())
+    _lib.call("qc64_hard_bits" if fp64 else "qc_hard_bits", plan.handle, gp, dev.data_ptr(),
+              hb.data_ptr(), _stream())
     if layout.edge_count:
         _lib.call("qc_syndrome", plan.handle, gp, hb.data_ptr(), bad.data_ptr(), _stream())
     bits = unpack_planes(hb.cpu().numpy().view(np.uint32), g)
@@ -160,7 +169,8 @@ class BlockDecoder:
     """
 
     def __init__(self, layout: EdgeLayout, gamma: int, iterations: int = 30,
-                 early_stop: bool = False, graph: bool = True, count_bits: bool = True):
+                 early_stop: bool = False, graph: bool = True, count_bits: bool = True,
+                 precision: str | None = None):
         torch = require_cuda()
         if iterations < 1:
             raise ValueError("need at least one iteration")
@@ -168,10 +178,11 @@ class BlockDecoder:
         self.early_stop = bool(early_stop)
         self.gp = pad32(gamma)
         self.plan = layout.plan()
+        self.fp64 = (precision or get_precision()) == "float64"
         dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         N, E, gp = layout.n_vars, max(layout.edge_count, 1), self.gp
-        f32, i32 = torch.float32, torch.int32
+        f32, i32 = (torch.float64 if self.fp64 else torch.float32), torch.int32
         self.mu = torch.full((N, gp), L_MAX, dtype=f32, device=dev)
         self.msgs = torch.zeros((E, gp), dtype=f32, device=dev)
         self.post = torch.zeros((N, gp), dtype=f32, device=dev)
@@ -187,6 +198,15 @@ class BlockDecoder:
 
     # -- device work ------------------------------------------------------
     def _launch(self):
+        if self.fp64:
+            _lib.call("qc64_decode", self.plan.handle, self.gp, self.iterations, int(self.early_stop),
+                      self.mu.data_ptr(), self.msgs.data_ptr(), self.post.data_ptr(),
+                      self.hb.data_ptr(), self.work.data_ptr(), self.ok.data_ptr(),
+                      self.iters.data_ptr(), _stream())
+            if self.lane_bits is not None:
+                _lib.call("qc_bit_errors", self.plan.handle, self.gp, self.hb.data_ptr(),
+                          self.lane_bits.data_ptr(), _stream())
+            return
         _lib.call("qc_decode", self.plan.handle, self.gp, self.iterations, int(self.early_stop),
                   self.mu.data_ptr(), self.msgs.data_ptr(), self.post.data_ptr(),
                   self.hb.data_ptr(), self.work.data_ptr(), self.ok.data_ptr(),
@@ -242,6 +262,10 @@ class BlockDecoder:
         if self._x is None or tuple(self._x.shape) != (gi, n):
             self._x = torch.empty((gi, n), dtype=torch.float64, device=self.device)
         self._x.copy_(h, non_blocking=True)
+        if self.fp64:
+            _lib.call("qc64_mu_from_lane_major", n, self.gp, gi, self._x.data_ptr(),
+                      float(sigma) if sigma is not None else 0.0, 1, self.mu.data_ptr(), _stream())
+            return
         _lib.call("qc_llr_from_lane_major", n, self.gp, gi, self._x.data_ptr(),
                   float(sigma) if sigma is not None else 0.0, self.mu.data_ptr(), _stream())
 
@@ -251,13 +275,14 @@ class BlockDecoder:
         computed in; hard bits; syndrome flags; iteration counts)."""
         import torch
         n = self.layout.n_vars
+        pdt = torch.float64 if self.fp64 else torch.float32
         if getattr(self, "_lm", None) is None or self._lm[0].shape[0] != gamma:
-            self._lm = (torch.empty((gamma, n), dtype=torch.float32, device=self.device),
+            self._lm = (torch.empty((gamma, n), dtype=pdt, device=self.device),
                         torch.empty((gamma, n), dtype=torch.uint8, device=self.device))
         post_d, bits_d = self._lm
-        _lib.call("qc_lane_major_f32", n, self.gp, gamma, self.post.data_ptr(), post_d.data_ptr(),
-                  bits_d.data_ptr(), _stream())
-        hp = self._pinned("post", (gamma, n), torch.float32)
+        _lib.call("qc64_lane_major" if self.fp64 else "qc_lane_major_f32", n, self.gp, gamma,
+                  self.post.data_ptr(), post_d.data_ptr(), bits_d.data_ptr(), _stream())
+        hp = self._pinned("post", (gamma, n), pdt)
         hb = self._pinned("bits", (gamma, n), torch.uint8)
         hs = self._pinned("small", (2, self.gp), torch.int32)
         hp.copy_(post_d, non_blocking=True)
@@ -336,7 +361,7 @@ def _pipelined(layout: EdgeLayout, x: np.ndarray, sigma, iterations: int, early_
 
 def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool, slot: int = 0) -> BlockDecoder:
     cache = layout.__dict__.setdefault("_decoders", {})
-    key = (pad32(gamma), iterations, bool(early_stop), slot)
+    key = (pad32(gamma), iterations, bool(early_stop), slot, get_precision())
     dec = cache.get(key)
     if dec is None:
         if len(cache) >= 8:

@@ -143,7 +143,9 @@ class BlockCampaign:
         self.layout, self.gref, self.units = layout, gamma_ref, units
         self.gk = gamma_ref * units
         self.k0, self.k1 = seed_words(seed)
-        self.dec = BlockDecoder(layout, self.gk, iterations, early_stop, graph=False, count_bits=True)
+        # campaigns run the fp32 production kernels (the channel writes fp32 LLRs)
+        self.dec = BlockDecoder(layout, self.gk, iterations, early_stop, graph=False, count_bits=True,
+                                precision="float32")
         dev = self.dec.device
         self.lane0 = torch.zeros(1, dtype=torch.int64, device=dev)
         self.counts = torch.zeros((units, 3), dtype=torch.int64, device=dev)

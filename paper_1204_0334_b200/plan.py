@@ -3,10 +3,27 @@
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
 from . import _lib
+
+# Message precision of the block decoder API: "float32" (production: phi-form
+# fp32 kernels) or "float64" (conformance build: the reference's tanh rule in
+# float64, csrc/block64.cu).  Campaigns and the stream decoder are fp32.
+_PRECISION = os.environ.get("QCLDPC_B200_PRECISION", "float32")
+
+
+def set_precision(p: str) -> None:
+    global _PRECISION
+    if p not in ("float32", "float64"):
+        raise ValueError("precision must be 'float32' or 'float64'")
+    _PRECISION = p
+
+
+def get_precision() -> str:
+    return _PRECISION
 
 
 def require_cuda():

@@ -12,7 +12,7 @@ HEADER = os.path.join(REPO, "include", "qcldpc_b200.h")
 
 def declared():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"QC_API\s+[\w\s\*]+?\b((?:qc|cc)_\w+)\s*\(", txt)))
+    return sorted(set(re.findall(r"QC_API\s+[\w\s\*]+?\b((?:qc64|qc|cc)_\w+)\s*\(", txt)))
 
 
 def test_header_declares_entry_points():

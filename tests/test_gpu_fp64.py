@@ -1,0 +1,136 @@
+"""GPU, float64 conformance build: the reference's own tests that need its
+1e-12 tolerances (restated from pkg/tests/test_bp.py and test_acceptance.py
+criteria 1, 3, 7), run against the drop-in API with set_precision("float64")."""
+import itertools
+
+import numpy as np
+import pytest
+from conftest import golden
+from scipy.special import logsumexp
+
+pytestmark = pytest.mark.gpu
+
+ALPHA_EXCLUSIVE = [-0.22733629380264572863, +0.37747645630979721384, -0.73532566405551922471]
+ALPHA_DEGREE1 = 28.324190418452803892
+
+
+@pytest.fixture
+def q64(gpu):
+    gpu.set_precision("float64")
+    yield gpu
+    gpu.set_precision("float32")
+
+
+def single(q, n):
+    return q.build_edge_layout(q.SparseParityCheck(n, [list(range(n))]))
+
+
+def test_kats_1e12(q64):
+    q = q64
+    lay = single(q, 3)
+    b = q.MessageBatch(lay, np.array([[2.0], [-1.0], [0.5]]))
+    q.check_node_update(b, lay)
+    assert np.allclose(b.packages[:, 0], ALPHA_EXCLUSIVE, atol=1e-12, rtol=0)
+    lay1 = single(q, 1)
+    b1 = q.MessageBatch(lay1, np.array([[3.0]]))
+    q.check_node_update(b1, lay1)
+    assert abs(b1.packages[0, 0] - ALPHA_DEGREE1) < 1e-12
+    lay2 = single(q, 2)
+    b2 = q.MessageBatch(lay2, np.array([[1.25], [-0.75]]))
+    q.check_node_update(b2, lay2)
+    assert np.allclose(b2.packages[:, 0], [-0.75, 1.25], atol=1e-12, rtol=0)
+
+
+def test_sign_rule_and_contraction(q64):
+    q = q64
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        d = int(rng.integers(3, 7))
+        lay = single(q, d)
+        beta = rng.normal(0, 2, size=(1, d))
+        b = q.MessageBatch(lay, beta.T.copy())
+        q.check_node_update(b, lay)
+        alpha = b.packages[:, 0]
+        for k in range(d):
+            others = np.delete(beta[0], k)
+            assert np.sign(alpha[k]) == np.prod(np.sign(others))
+            assert abs(alpha[k]) <= np.min(np.abs(others)) + 1e-12
+
+
+def test_exclusive_sum_consistency_bulk(q64):
+    q = q64
+    lay = q.build_edge_layout(q.SparseParityCheck(8, [[0, 1, 2, 3], [2, 3, 4, 5], [4, 5, 6, 7]]))
+    rng = np.random.default_rng(11)
+    mu = rng.normal(0, 3, size=(300, 8))
+    mu[:20] = 49.0
+    b = q.MessageBatch(lay, mu.T.copy())
+    for _ in range(6):
+        q.check_node_update(b, lay)
+        alpha = b.packages.copy()
+        post = q.variable_node_update(b, lay)
+        assert np.all(np.abs(alpha) <= 50) and np.all(np.abs(b.packages) <= 50)
+        for v, edges in enumerate(lay.var_edges):
+            for e in edges:
+                beta = b.packages[e]
+                free = (np.abs(beta) < 50) & (np.abs(post[v]) < 50)
+                err = np.abs(post[v, free] - beta[free] - alpha[e, free])
+                assert err.size == 0 or err.max() < 1e-12
+
+
+def _exact_posterior(rows, n, mu):
+    """Enumeration over all 2^n words (restates reference.py:25-60)."""
+    words = (np.arange(1 << n)[:, None] >> np.arange(n)) & 1
+    valid = np.ones(1 << n, bool)
+    for cols in rows:
+        valid &= (words[:, cols].sum(axis=1) & 1) == 0
+    w = words[valid]
+    logw = -(w @ mu)
+    return np.array([logsumexp(logw[w[:, i] == 0]) - logsumexp(logw[w[:, i] == 1]) for i in range(n)])
+
+
+def test_trees_equal_enumeration(q64):
+    q = q64
+    rng = np.random.default_rng(100)
+    worst = 0.0
+    for _ in range(10):
+        rows, n = [], 1
+        while True:
+            fresh = int(rng.integers(1, 3))
+            if n + fresh > 12:
+                break
+            rows.append([int(rng.integers(0, n))] + list(range(n, n + fresh)))
+            n += fresh
+            if len(rows) >= 3 and rng.random() < 0.25:
+                break
+        lay = q.build_edge_layout(q.SparseParityCheck(n, rows))
+        mu = rng.normal(0.0, 1.5, size=n)
+        r = q.decode_llr_batch(lay, mu[None, :], 2 * (n + len(rows)))
+        worst = max(worst, float(np.abs(r.posteriors[0] - _exact_posterior(rows, n, mu)).max()))
+    assert worst < 1e-9
+
+
+def test_toy_golden_fp64(q64):
+    q = q64
+    g = golden("block_toy.npz")
+    lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30)
+    assert np.array_equal(r.hard_bits, g["bits30"]) and np.array_equal(r.syndrome_ok, g["ok30"])
+    assert np.allclose(r.posteriors, g["post30"], rtol=1e-12, atol=1e-12)
+    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30, early_stop=True)
+    assert np.array_equal(r.iterations_run, g["iters_es"])
+    assert np.allclose(r.posteriors, g["post_es"], rtol=1e-12, atol=1e-12)
+    mu = q.channel_llrs(g["y"], float(g["sigma"]))
+    b = q.MessageBatch(lay, np.ascontiguousarray(mu.T))
+    q.check_node_update(b, lay)
+    assert np.allclose(b.packages, g["cnu1"], rtol=1e-12, atol=1e-13)
+
+
+def test_wide_batch_bit_exact_fp64(q64):
+    q = q64
+    lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    rng = np.random.default_rng(300)
+    for _ in range(10):
+        y = rng.normal(1.0, 1.0, size=(1, lay.n_vars))
+        one = q.decode_batch(lay, y, 1.0, 6)
+        wide = q.decode_batch(lay, np.repeat(y, 32, axis=0), 1.0, 6)
+        assert np.array_equal(np.repeat(one.posteriors, 32, axis=0), wide.posteriors)
