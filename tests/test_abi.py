@@ -54,17 +54,8 @@ def test_product_path_does_not_import_oracle():
             assert "import oracle" not in src and "from oracle" not in src, f
 
 
-def test_missing_library_fails_loudly(tmp_path):
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     from paper_1204_0334_b200 import _lib
+    monkeypatch.setattr(_lib, "_LIB", None)
     with pytest.raises(_lib.LibraryMissing):
-        _lib.load.__wrapped__(str(tmp_path / "nope.so")) if hasattr(_lib.load, "__wrapped__") else \
-            _raise_missing(_lib, str(tmp_path / "nope.so"))
-
-
-def _raise_missing(_lib, path):
-    saved = _lib._LIB
-    try:
-        _lib._LIB = None
-        _lib.load(path)
-    finally:
-        _lib._LIB = saved
+        _lib.load(str(tmp_path / "nope.so"))

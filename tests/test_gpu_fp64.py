@@ -110,19 +110,28 @@ def test_trees_equal_enumeration(q64):
 
 
 def test_toy_golden_fp64(q64):
+    """One update of each kind agrees with the reference to 1e-12; over 30
+    iterations the CUDA-vs-numpy tanh/atanh ulps amplify (messages saturate,
+    trajectories stay identical), so the full decode is held to 1e-9 relative
+    with bit-exact decisions."""
     q = q64
     g = golden("block_toy.npz")
     lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
-    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30)
-    assert np.array_equal(r.hard_bits, g["bits30"]) and np.array_equal(r.syndrome_ok, g["ok30"])
-    assert np.allclose(r.posteriors, g["post30"], rtol=1e-12, atol=1e-12)
-    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30, early_stop=True)
-    assert np.array_equal(r.iterations_run, g["iters_es"])
-    assert np.allclose(r.posteriors, g["post_es"], rtol=1e-12, atol=1e-12)
     mu = q.channel_llrs(g["y"], float(g["sigma"]))
     b = q.MessageBatch(lay, np.ascontiguousarray(mu.T))
     q.check_node_update(b, lay)
-    assert np.allclose(b.packages, g["cnu1"], rtol=1e-12, atol=1e-13)
+    assert np.allclose(b.packages, g["cnu1"], rtol=1e-12, atol=1e-12)
+    post1 = q.variable_node_update(b, lay)
+    assert np.allclose(post1, g["post1"], rtol=1e-12, atol=1e-12)
+    assert np.allclose(b.packages, g["vnu1"], rtol=1e-12, atol=1e-12)
+    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30)
+    assert np.array_equal(r.hard_bits, g["bits30"]) and np.array_equal(r.syndrome_ok, g["ok30"])
+    err = np.abs(r.posteriors - g["post30"]) / np.maximum(np.abs(g["post30"]), 1.0)
+    assert err.max() < 1e-9, err.max()
+    r = q.decode_batch(lay, g["y"], float(g["sigma"]), 30, early_stop=True)
+    assert np.array_equal(r.iterations_run, g["iters_es"]) and np.array_equal(r.hard_bits, g["bits_es"])
+    err = np.abs(r.posteriors - g["post_es"]) / np.maximum(np.abs(g["post_es"]), 1.0)
+    assert err.max() < 1e-9, err.max()
 
 
 def test_wide_batch_bit_exact_fp64(q64):
