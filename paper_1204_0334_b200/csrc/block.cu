@@ -21,9 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstring>
-#include <mutex>
 #include <string>
 #include <vector>
 
@@ -43,7 +41,8 @@ __global__ void init_kernel(const float* mu, float* msgs, const int32_t* edge_va
   vstore<4>(msgs + (size_t)e * gamma + q * 4, v);
 }
 
-template <int DC>
+// per (check, 32-lane word): XOR of the hard-bit planes of the check's
+// variables; any odd word marks its lanes as failing (bp.py:199-208)
 __global__ void syndrome_kernel(const uint32_t* hb, uint32_t* bad, const int32_t* check_ptr,
                                 const int32_t* edge_var, int M, int W, const int32_t* done) {
   if (done && *done) return;
@@ -238,7 +237,7 @@ int launch_syndrome(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* b
   int W = gamma / 32;
   if (p->M == 0) return 0;
   long long threads = (long long)p->M * W;
-  syndrome_kernel<0><<<blocks_for(threads), THREADS, 0, s>>>(hb, bad, p->d_check_ptr, p->d_edge_var, p->M, W, done);
+  syndrome_kernel<<<blocks_for(threads), THREADS, 0, s>>>(hb, bad, p->d_check_ptr, p->d_edge_var, p->M, W, done);
   return check_launch("syndrome");
 }
 

@@ -235,6 +235,10 @@ inline int pick_vec_vnu(int gamma) {
 
 QcGrid make_grid(const qc_plan* p);
 
+// persistent cp.async-pipelined check pass (cnu_pipe.cu); 0 if not applicable
+int launch_cnu_phi_pipe(const qc_plan* p, const CnuArgs& a, cudaStream_t s);
+int cnu_pipe_mode();   // QCB_CNU_PIPE env: 1 = use the pipelined check pass
+
 template <int DC>
 int launch_cnu_dc(const qc_plan* p, const CnuArgs& a, int mode, cudaStream_t s);
 

@@ -219,3 +219,31 @@ def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
     close(r.posteriors, post)
     r2 = q.decode_batch(lay, y[:64], 1.0, 12)
     assert np.array_equal(r2.posteriors, r.posteriors[:64])
+
+
+_PIPE_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+import paper_1204_0334_b200 as q
+h, exp = q.load_code(q.codes.bundled_code_path('n18360'))
+lay = q.build_edge_layout(h)
+y = q.simulate_block(q.ChannelConfig(2.9, 5 / 6, seed=4, gamma=512), lay.n_vars)
+r = q.decode_batch(lay, y, q.ebn0_to_sigma(2.9, 5 / 6), 30)
+np.save(sys.argv[1], r.posteriors)
+"""
+
+
+def test_pipelined_check_pass_is_bit_identical(gpu, tmp_path):
+    """QCB_CNU_PIPE=1 selects the persistent cp.async check pass: same arithmetic,
+    bit-identical posteriors."""
+    import os
+    import subprocess
+    import sys
+    from conftest import REPO
+    outs = []
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"post_{mode}.npy")
+        env = dict(os.environ, QCB_CNU_PIPE=mode)
+        subprocess.run([sys.executable, "-c", _PIPE_SNIPPET, f], cwd=REPO, env=env, check=True)
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
