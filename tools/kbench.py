@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--gammas", type=int, nargs="+", default=[1024])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--code", default="n18360")
+    ap.add_argument("--early-stop", action="store_true", help="time the early-stop decode (per-lane freeze)")
+    ap.add_argument("--ebn0", type=float, default=3.2)
     args = ap.parse_args()
     import torch
     import paper_1204_0334_b200 as q
@@ -28,8 +30,8 @@ def main():
     N, E = lay.n_vars, lay.edge_count
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
     for G in args.gammas:
-        dec = q.BlockDecoder(lay, G, 30, graph=False)
-        sigma = q.ebn0_to_sigma(3.2, 1 - lay.n_checks / N)
+        dec = q.BlockDecoder(lay, G, 30, early_stop=args.early_stop, graph=False)
+        sigma = q.ebn0_to_sigma(args.ebn0, 1 - lay.n_checks / N)
         _lib.call("qc_channel", 0, 0, 0, 0, N, G, sigma, dec.mu.data_ptr(), None, None, 0)
         st = _lib.stream_handle()
         p = dec.plan.handle
@@ -53,6 +55,7 @@ def main():
         vnu_phi = timeit(lambda: _lib.call("qc_vnu_ex", p, G, 1, dec.msgs.data_ptr(), dec.mu.data_ptr(), None,
                                            None, None, st))
         dec_ms = timeit(dec.run, max(3, args.reps // 4))
+        mean_it = float(dec.iters[:G].float().mean().item())
         cb, vb = 2 * E * G * 4, (2 * E + N) * G * 4
         alg = 4 * (30 * (4 * E + N) + (N + E)) * G
         print(json.dumps({
@@ -62,7 +65,8 @@ def main():
             "vnu_phi_ms": round(vnu_phi, 4), "vnu_phi_gbs": round(vb / vnu_phi / 1e6, 1),
             "decode_ms": round(dec_ms, 3), "decode_alg_gbs": round(alg / dec_ms / 1e6, 1),
             "decode_frac": round(alg / dec_ms / 1e6 / peak, 4),
-            "mbit_s": round(G * (N - lay.n_checks) / dec_ms / 1e3, 1)}), flush=True)
+            "mbit_s": round(G * (N - lay.n_checks) / dec_ms / 1e3, 1),
+            "early_stop": args.early_stop, "ebn0_db": args.ebn0, "mean_iterations": round(mean_it, 2)}), flush=True)
         del dec
         torch.cuda.empty_cache()
 
