@@ -110,6 +110,24 @@ QC_API int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post,
 QC_API int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma,
                                   float* mu_vm, void* stream);
 
+/* ---- lane-recycling early-stop campaign engine (harness.py:144-204 with
+ * early_stop=True): a lane whose codeword froze (bp.py:242-256) or hit the
+ * iteration cap immediately starts codeword next_id; per-codeword results and
+ * per-batch counters equal the reference's.  Regular (J, 24) QC grids,
+ * gamma % 64 == 0.  state: qc_rc_state_bytes(gamma) bytes of device memory. */
+QC_API size_t qc_rc_state_bytes(int gamma);
+QC_API int qc_rc_init(int gamma, int64_t id_limit, void* state, void* stream);
+/* run `ticks` flooding iterations of every busy lane; codeword id k of this rank
+ * is reference batch (k / gamma_ref) * world + rank, lane lane_base + batch *
+ * gamma_ref + k % gamma_ref; finished codewords add (1, bit errors, frame
+ * error) to counts[batch] (n_batches x 3 int64). */
+QC_API int qc_rc_ticks(const qc_plan* plan, int gamma, int gamma_ref, int world, int rank, int max_it,
+                       int64_t id_limit, int64_t n_batches, uint64_t seed_lo, uint64_t seed_hi,
+                       uint64_t lane_base, double sigma, int ticks, float* mu, float* msgs, uint32_t* hb,
+                       void* state, int64_t* counts, void* stream);
+/* copy the next codeword id (progress) to a device int64 */
+QC_API int qc_rc_next_id(int gamma, const void* state, int64_t* next_id_dev_out, void* stream);
+
 /* ---- float64 conformance build (block decoder) ---------------------------
  * The reference's own arithmetic (tanh rule with sequential forward/backward
  * products, bp.py:120-188) in float64 on the GPU, for callers relying on the

@@ -361,7 +361,8 @@ def _pipelined(layout: EdgeLayout, x: np.ndarray, sigma, iterations: int, early_
 
 def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool, slot: int = 0) -> BlockDecoder:
     cache = layout.__dict__.setdefault("_decoders", {})
-    key = (pad32(gamma), iterations, bool(early_stop), slot, get_precision())
+    import torch
+    key = (pad32(gamma), iterations, bool(early_stop), slot, get_precision(), torch.cuda.current_device())
     dec = cache.get(key)
     if dec is None:
         if len(cache) >= 8:

@@ -152,7 +152,7 @@ class EdgeLayout:
         self.check_pad = check_pad
         self.var_pad = var_pad
         self.qc = qc
-        self._plan = None
+        self._plans = {}
 
     @property
     def n_checks(self) -> int:
@@ -166,11 +166,13 @@ class EdgeLayout:
         return np.arange(self.check_ptr[m], self.check_ptr[m + 1], dtype=np.int64)
 
     def plan(self):
-        """Device plan (created on first use, shared, immutable)."""
-        if self._plan is None:
-            from .plan import BlockPlan
-            self._plan = BlockPlan(self)
-        return self._plan
+        """Device plan of the current CUDA device (created on first use, immutable)."""
+        import torch
+        from .plan import BlockPlan
+        dev = torch.cuda.current_device()
+        if dev not in self._plans:
+            self._plans[dev] = BlockPlan(self)
+        return self._plans[dev]
 
     def __repr__(self):
         return (f"EdgeLayout(N={self.n_vars}, M={self.n_checks}, E={self.edge_count}, "

@@ -52,7 +52,7 @@ class LdpcccCode:
                                        dtype=np.int64)
         self.sub_offset = np.concatenate([[0], np.cumsum(self.sub_edge_count)[:-1]]).astype(np.int64)
         self.edge_count = int(self.sub_edge_count.sum())
-        self._plan = None
+        self._plans = {}
 
     @property
     def period(self) -> int:
@@ -63,12 +63,15 @@ class LdpcccCode:
         return (self.c - self.cb) / self.c
 
     def plan(self) -> StreamPlan:
-        if self._plan is None:
-            self._plan = StreamPlan(self.exp)
-            if (self._plan.E != self.edge_count or self._plan.c != self.c
-                    or self._plan.lam != self.lam):
+        """Device plan of the current CUDA device (created on first use, immutable)."""
+        import torch
+        dev = torch.cuda.current_device()
+        if dev not in self._plans:
+            pl = StreamPlan(self.exp)
+            if pl.E != self.edge_count or pl.c != self.c or pl.lam != self.lam:
                 raise RuntimeError("device LDPCCC plan does not match the host tables")
-        return self._plan
+            self._plans[dev] = pl
+        return self._plans[dev]
 
 
 def unwrap_qc(exp: ExponentMatrix) -> LdpcccCode:

@@ -252,6 +252,15 @@ int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* 
 
 }  // namespace
 
+namespace qcb {
+int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s) {
+  return launch_syndrome(p, gamma, hb, bad, nullptr, s);
+}
+int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s) {
+  return launch_bit_errors(p, gamma, hb, lane_bits, s);
+}
+}  // namespace qcb
+
 // ============================================================================
 // C ABI
 // ============================================================================

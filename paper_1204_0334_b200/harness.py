@@ -40,7 +40,7 @@ from .plan import require_cuda
 __all__ = [
     "SimulationConfig", "PointResult", "CSV_COLUMNS", "run_block_simulation",
     "run_stream_simulation", "bench_throughput", "write_csv", "write_jsonl",
-    "BlockCampaign", "StreamCampaign",
+    "BlockCampaign", "StreamCampaign", "RecycleCampaign",
 ]
 
 CSV_COLUMNS = [
@@ -184,12 +184,99 @@ class BlockCampaign:
         self._graph.replay()
 
 
+class RecycleCampaign:
+    """Lane-recycling early-stop engine (csrc/recycle.cu) for regular (J, 24) QC codes.
+
+    gamma_kernel lanes ("slots") decode codewords continuously: a slot whose
+    codeword froze (syndrome clean) or reached the iteration cap takes the next
+    codeword id at once, so the GPU always works on dense lanes.  Codeword k of
+    rank r is lane lane_base + b*gref + k % gref of reference batch
+    b = (k // gref) * W + r; per-batch counters are exactly the reference's
+    early-stop counts (harness.py:144-154 with early_stop=True).
+    """
+
+    TICKS = 16
+
+    def __init__(self, layout: EdgeLayout, gamma_ref: int, gamma_kernel: int, iterations: int, seed: int,
+                 rank: int, world_size: int):
+        torch = require_cuda()
+        self.layout, self.gref, self.gk, self.iters = layout, gamma_ref, gamma_kernel, iterations
+        self.rank, self.W = rank, world_size
+        self.k0, self.k1 = seed_words(seed)
+        self.plan = layout.plan()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        N, E = layout.n_vars, layout.edge_count
+        self.mu = torch.zeros((N, self.gk), dtype=torch.float32, device=dev)
+        self.msgs = torch.zeros((E, self.gk), dtype=torch.float32, device=dev)
+        self.hb = torch.zeros((N, self.gk // 32), dtype=torch.int32, device=dev)
+        nbytes = int(_lib.load().qc_rc_state_bytes(self.gk))
+        self.state = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        self.next_id = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._graph = None
+        self._key = None
+
+    @staticmethod
+    def supports(layout: EdgeLayout) -> bool:
+        return layout.qc is not None and bool((layout.qc.shifts >= 0).all()) and layout.check_regular == 24
+
+    def _ticks(self, sigma, lane_base, id_limit, n_batches, counts):
+        _lib.call("qc_rc_ticks", self.plan.handle, self.gk, self.gref, self.W, self.rank, self.iters,
+                  int(id_limit), int(n_batches), self.k0, self.k1, int(lane_base), float(sigma), self.TICKS,
+                  self.mu.data_ptr(), self.msgs.data_ptr(), self.hb.data_ptr(), self.state.data_ptr(),
+                  counts.data_ptr(), _lib.stream_handle())
+        _lib.call("qc_rc_next_id", self.gk, self.state.data_ptr(), self.next_id.data_ptr(),
+                  _lib.stream_handle())
+
+    def run_point(self, sigma: float, lane_base: int, stop: int, max_frames: int, group=None):
+        """Decode until the ordered stop rule is met; returns (frames, bit_errors, frame_errors)."""
+        import torch
+        W, gref = self.W, self.gref
+        n_batches = -(-max_frames // gref)                 # global batch rows
+        local_batches = -(-n_batches // W) if n_batches > self.rank else 0
+        id_limit = max(0, min(local_batches, -(-(n_batches - self.rank) // W))) * gref
+        counts = torch.zeros((n_batches + W, 3), dtype=torch.int64, device=self.mu.device)
+        _lib.call("qc_rc_init", self.gk, int(id_limit), self.state.data_ptr(), _lib.stream_handle())
+        key = (sigma, lane_base, id_limit, n_batches, counts.data_ptr())
+        self._graph = None
+        tot, done, scan = (0, 0, 0), False, 0
+        # only a window of batches after the consumed prefix can be in flight
+        win = 4 * (self.gk // gref + 1) * W + 64
+        while not done:
+            if self._graph is None:
+                self._ticks(sigma, lane_base, id_limit, n_batches, counts)      # eager first round
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._ticks(sigma, lane_base, id_limit, n_batches, counts)
+                self._graph, self._key = g, key
+            else:
+                self._graph.replay()
+            end = min(n_batches, scan + win)
+            red = counts[scan:end].clone()
+            sum_counts(red, group)
+            rows = red.cpu().numpy()
+            # consume the prefix of complete batches in order (harness.py:173-192)
+            hi = 0
+            while hi < rows.shape[0] and rows[hi, 0] == gref:
+                hi += 1
+            tot, done, used = ordered_prefix(rows[:hi], stop, max_frames, tot)
+            scan += used
+            if not done and scan >= n_batches:
+                done = True
+        torch.cuda.synchronize()
+        return tot
+
+
 def run_block_simulation(layout: EdgeLayout, config: SimulationConfig, *,
-                         gamma_kernel: int | None = None, group=None) -> list:
-    """Sweep the Eb/N0 points with the GPU block decoder (harness.py:157-204)."""
+                         gamma_kernel: int | None = None, group=None, recycle: bool | None = None) -> list:
+    """Sweep the Eb/N0 points with the GPU block decoder (harness.py:157-204).
+
+    early_stop campaigns on regular (J, 24) QC codes use lane recycling
+    (`RecycleCampaign`, identical counts) unless recycle=False."""
     torch = require_cuda()
     rank, W, g = world() if group is None else (torch.distributed.get_rank(group),
                                                  torch.distributed.get_world_size(group), group)
+    if config.early_stop and (recycle if recycle is not None else RecycleCampaign.supports(layout)):
+        return _run_block_recycled(layout, config, gamma_kernel, rank, W, g)
     rate = 1.0 - layout.n_checks / layout.n_vars
     info_bits = layout.n_vars - layout.n_checks
     gref = config.gamma
@@ -218,6 +305,29 @@ def run_block_simulation(layout: EdgeLayout, config: SimulationConfig, *,
         results.append(PointResult(
             code_id=config.code_id, mode="block", ebn0_db=db, iters_or_i=config.iterations,
             gamma=gref, frames=frames, bit_errors=be, frame_errors=fe,
+            ber=be / (frames * layout.n_vars) if frames else 0.0,
+            fer=fe / frames if frames else 0.0, seconds=dt,
+            frames_per_sec=frames / dt if dt else 0.0,
+            info_bits_per_sec=frames * info_bits / dt if dt else 0.0))
+    return results
+
+
+def _run_block_recycled(layout, config, gamma_kernel, rank, W, g):
+    import torch
+    rate = 1.0 - layout.n_checks / layout.n_vars
+    info_bits = layout.n_vars - layout.n_checks
+    gk = max(64, (gamma_kernel or 4096) // 64 * 64)
+    eng = RecycleCampaign(layout, config.gamma, gk, config.iterations, config.seed, rank, W)
+    results = []
+    for pi, db in enumerate(config.points()):
+        sigma = ebn0_to_sigma(db, rate)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        frames, be, fe = eng.run_point(sigma, pi << 32, config.stop_block_errors, config.max_frames, g)
+        dt = time.perf_counter() - t0
+        results.append(PointResult(
+            code_id=config.code_id, mode="block", ebn0_db=db, iters_or_i=config.iterations,
+            gamma=config.gamma, frames=frames, bit_errors=be, frame_errors=fe,
             ber=be / (frames * layout.n_vars) if frames else 0.0,
             fer=fe / frames if frames else 0.0, seconds=dt,
             frames_per_sec=frames / dt if dt else 0.0,

@@ -113,3 +113,21 @@ def test_block_campaign_odd_n_vs_oracle(gpu):
     want = campaign.block_point(oqc.qc_layout(oqc.array_code_shifts(3, 7, 11), 11), 2.0, 0, iters=10,
                                 gamma=16, seed=11, stop=20, max_frames=3000)
     assert (r.frames, r.bit_errors, r.frame_errors) == want
+
+
+def test_recycled_early_stop_campaign_matches_oracle(gpu, codes_npz):
+    """Lane recycling (early_stop campaigns) gives the reference's early-stop counts."""
+    from oracle import campaign, qc as oqc
+    q = gpu
+    sh, p = codes_npz["code_a_shifts"], int(codes_npz["code_a_p"])
+    lay = q.build_edge_layout(q.expand_qc(q.ExponentMatrix(sh, p)))
+    assert q.RecycleCampaign.supports(lay)
+    cfg = q.SimulationConfig("code-a", [3.0], iterations=30, gamma=32, stop_block_errors=4,
+                             max_frames=640, seed=3, early_stop=True)
+    r = q.run_block_simulation(lay, cfg, gamma_kernel=128)[0]
+    want = campaign.block_point(oqc.qc_layout(sh, p), 3.0, 0, iters=30, gamma=32, seed=3, stop=4,
+                                max_frames=640, early_stop=True)
+    assert (r.frames, r.bit_errors, r.frame_errors) == want
+    # the non-recycled early-stop path agrees too
+    r2 = q.run_block_simulation(lay, cfg, gamma_kernel=128, recycle=False)[0]
+    assert (r2.frames, r2.bit_errors, r2.frame_errors) == want
