@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--ebn0", type=float, nargs="+", default=[3.0, 3.2, 3.4, 3.6])
     ap.add_argument("--frames", type=int, default=65536)
     ap.add_argument("--gamma-kernel", type=int, default=4096)
+    ap.add_argument("--modes", nargs="+", default=["fixed30", "early_stop", "recycled"])
     args = ap.parse_args()
     import paper_1204_0334_b200 as q
     h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
@@ -24,6 +25,8 @@ def main():
     for db in args.ebn0:
         row = {"ebn0_db": db, "frames": args.frames}
         for name, es, rec in (("fixed30", False, None), ("early_stop", True, False), ("recycled", True, True)):
+            if name not in args.modes:
+                continue
             cfg = q.SimulationConfig("n18360", [db], iterations=30, gamma=32, stop_block_errors=2**62,
                                      max_frames=args.frames, seed=0, early_stop=es)
             q.run_block_simulation(lay, cfg, gamma_kernel=args.gamma_kernel, recycle=rec)   # warm-up
