@@ -253,6 +253,7 @@ int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* 
 }  // namespace
 
 namespace qcb {
+int launch_cnu_public(const qc_plan* p, CnuArgs a, int mode, cudaStream_t s) { return launch_cnu(p, a, mode, s); }
 int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s) {
   return launch_syndrome(p, gamma, hb, bad, nullptr, s);
 }

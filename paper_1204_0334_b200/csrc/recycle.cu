@@ -1,38 +1,48 @@
-// Lane-recycling early-stop Monte-Carlo engine for regular QC block codes.
+// Sector-granular lane-recycling early-stop Monte-Carlo engine (block codes).
 //
 // The reference's early-stop campaign (harness.py:144-154 with
-// SimulationConfig.early_stop, bp.py:242-256) decodes each batch of gamma
-// codewords until every lane's syndrome clears or the iteration cap is hit;
-// on a GPU that leaves the late, sparse lanes scattered over every package, so
-// the memory traffic barely drops.  Here a lane ("slot") whose codeword has
-// frozen immediately takes the next codeword id and restarts from its channel
-// LLRs, so every tick (one flooding iteration of all slots) does dense work.
-// Each codeword still runs exactly the reference's early-stop schedule on its
-// own lane (lanes never interact), so per-codeword bits / errors and therefore
-// the per-batch counters are identical; only the tick in which a codeword is
-// decoded changes.
+// SimulationConfig.early_stop, bp.py:242-256) decodes a batch until every
+// lane's syndrome clears or the iteration cap is hit.  On a GPU that leaves
+// straggler lanes scattered over every package: a 32-byte sector stays live
+// while any of its 8 lanes is, so memory traffic barely drops.  Here lanes are
+// recycled in groups of 8 (one sector): when all 8 codewords of a group have
+// frozen (or hit the cap), the group immediately starts the next 8 codeword
+// ids.  Fresh groups get their channel LLRs and beta^0 = mu written densely
+// (sector-aligned) from a compact list, and the tuned check / variable passes
+// run unchanged under the active-lane mask.  Each codeword still runs exactly
+// the reference's early-stop schedule on its own lane (lanes never interact),
+// so per-codeword results and the per-batch counters are identical; only the
+// tick in which a codeword is decoded changes.
 //
-// Codeword id k of this rank maps to reference batch b = (k / gref) * W + rank
-// and lane lane_base + b * gref + k % gref (batches round-robin over W ranks).
-// Per tick: channel (fresh slots) -> check pass (fresh slots read mu) ->
-// variable pass (phi form + hard-bit planes) -> syndrome -> per-slot bit
-// counts -> finish (count, reassign).
+// Codeword id k of this rank is reference batch b = (k / gref) * W + rank,
+// lane lane_base + b * gref + k % gref (batches round-robin over W ranks).
+// Tick = fresh-group channel -> fresh-group init -> check pass -> variable
+// pass -> syndrome -> per-lane bit counts -> finish (count, freeze, reassign).
 #include <cuda_runtime.h>
 
 #include "block_kernels.cuh"
 #include "philox.cuh"
 
 namespace qcb {
+
+int launch_vnu(const qc_plan* p, VnuArgs a, int mode, cudaStream_t s);
+int launch_cnu_public(const qc_plan* p, CnuArgs a, int mode, cudaStream_t s);
+int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s);
+int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s);
+
 namespace {
 
+constexpr int GROUP = 8;        // lanes per recycling group = one 32-byte sector of fp32
+
 struct RcState {
-  int64_t* slot_cw;        // (gamma) codeword id or -1
+  int64_t* slot_cw;        // (gamma) codeword id, -1 = none
   int32_t* slot_it;        // (gamma) iterations done
-  uint32_t* fresh;         // (W) slots that start a codeword this tick
-  uint32_t* active;        // (W) slots holding a codeword
-  uint32_t* bad;           // (W) syndrome failures of this tick
   int32_t* lane_bits;      // (gamma) hard-bit count of this tick
-  int64_t* next_id;        // [1] next codeword id to hand out
+  int32_t* fresh_list;     // (gamma / GROUP) groups starting this tick
+  int32_t* fresh_count;    // [1]
+  uint32_t* active;        // (W) lanes still iterating
+  uint32_t* bad;           // (W) syndrome failures of this tick
+  int64_t* next_group;     // [1] next group of codeword ids to hand out
   int64_t* counts;         // (n_batches, 3) frames, bit errors, frame errors
 };
 
@@ -50,88 +60,89 @@ __device__ __forceinline__ uint64_t ref_lane(const RcConfig& c, int64_t k) {
 }
 
 __global__ void rc_init_kernel(RcState s, RcConfig c) {
-  int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < c.gamma) {
-    int64_t k = g < c.id_limit ? g : -1;
-    s.slot_cw[g] = k;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = g < c.gamma;
+  const bool on = valid && g < c.id_limit;
+  if (valid) {
+    s.slot_cw[g] = on ? g : -1;
     s.slot_it[g] = 0;
+    if (g % GROUP == 0) s.fresh_list[g / GROUP] = g / GROUP;
   }
-  if (g < c.gamma / 32) {
-    uint32_t on = 0;
-    for (int b = 0; b < 32; ++b)
-      if (g * 32 + b < c.id_limit) on |= 1u << b;
-    s.fresh[g] = on;
-    s.active[g] = on;
-    s.bad[g] = 0;
+  const unsigned w = __ballot_sync(0xffffffffu, on);
+  if (valid && (g & 31) == 0) {
+    s.active[g >> 5] = w;
+    s.bad[g >> 5] = 0;
   }
-  if (g == 0) *s.next_id = c.gamma < c.id_limit ? c.gamma : c.id_limit;
+  if (g == 0) {
+    const int64_t groups = c.gamma / GROUP;
+    const int64_t lim = (c.id_limit + GROUP - 1) / GROUP;
+    *s.fresh_count = (int32_t)(groups < lim ? groups : lim);
+    *s.next_group = groups;
+  }
 }
 
-// channel LLRs of fresh slots only (thread = (slot g, Philox block of 4 positions))
+// channel LLRs of the fresh groups: item = (fresh group, Philox block, lane in group)
 __global__ void __launch_bounds__(THREADS) rc_channel_kernel(RcState s, RcConfig c, float* mu, int n) {
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int F = *s.fresh_count;
   const long long nblk = (n + 3) / 4;
-  if (tid >= nblk * c.gamma) return;
-  const int g = (int)(tid % c.gamma);
-  if (!((s.fresh[g >> 5] >> (g & 31)) & 1u)) return;
-  const long long b = tid / c.gamma;
-  uint64_t w[4];
-  philox4x64_10((uint64_t)b + 1ull, ref_lane(c, s.slot_cw[g]), 0ull, 0ull, c.k0, c.k1, w);
-  const double s2 = __dmul_rn(c.sigma, c.sigma);
+  const long long items = (long long)F * nblk * GROUP;
+  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(it % GROUP);
+    const long long r = it / GROUP;
+    const long long b = r % nblk;
+    const int g = s.fresh_list[r / nblk] * GROUP + l;
+    const int64_t k = s.slot_cw[g];
+    if (k < 0) continue;
+    uint64_t w[4];
+    philox4x64_10((uint64_t)b + 1ull, ref_lane(c, k), 0ull, 0ull, c.k0, c.k1, w);
+    const double s2 = __dmul_rn(c.sigma, c.sigma);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const long long pos = b * 4 + k;
-    if (pos >= n) break;
-    double y = __dadd_rn(1.0, __dmul_rn(c.sigma, ndtri_cephes(word_to_uniform(w[k]))));
-    double m = __ddiv_rn(__dmul_rn(2.0, y), s2);
-    m = m < -50.0 ? -50.0 : (m > 50.0 ? 50.0 : m);
-    mu[(size_t)pos * c.gamma + g] = __double2float_rn(m);
-  }
-}
-
-// check pass, phi form; fresh lanes take beta^0 = mu (fused init), idle lanes skip
-template <int DC, int VEC>
-__global__ void __launch_bounds__(THREADS) rc_cnu_kernel(CnuArgs a, const __grid_constant__ QcGrid grid,
-                                                        const uint32_t* fresh) {
-  const int GV = a.gamma / VEC;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)a.M * GV) return;
-  int m = (int)(tid / GV), q = (int)(tid - (long long)m * GV);
-  const unsigned lanes = lane_bits_of(a.active, q * VEC, VEC);
-  if (lanes == 0) return;
-  const unsigned fr = lane_bits_of(fresh, q * VEC, VEC) & lanes;
-  const int e0 = m * DC;
-  float x[DC][VEC];
-#pragma unroll
-  for (int k = 0; k < DC; ++k) vload<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
-  if (fr) {
-    const int jrow = m / grid.p, r = m - jrow * grid.p;
-#pragma unroll
-    for (int k = 0; k < DC; ++k) {
-      int c = r + grid.s[jrow * grid.L + k];
-      c -= (c >= grid.p) ? grid.p : 0;
-      float mv[VEC];
-      vload<VEC>(a.mu + (size_t)(k * grid.p + c) * a.gamma + q * VEC, mv);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i)
-        if ((fr >> i) & 1u)
-          x[k][i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(mv[i]))) |
-                                    (__float_as_uint(mv[i]) & 0x80000000u));
+    for (int q = 0; q < 4; ++q) {
+      const long long pos = b * 4 + q;
+      if (pos >= n) break;
+      double y = __dadd_rn(1.0, __dmul_rn(c.sigma, ndtri_cephes(word_to_uniform(w[q]))));
+      double m = __ddiv_rn(__dmul_rn(2.0, y), s2);
+      m = m < -50.0 ? -50.0 : (m > 50.0 ? 50.0 : m);
+      mu[(size_t)pos * c.gamma + g] = __double2float_rn(m);
     }
   }
-  cnu_core<DC, VEC, true>(x, DC, lanes);
-#pragma unroll
-  for (int k = 0; k < DC; ++k) vstore<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
 }
 
-// finish: count frozen / capped codewords into their batch, hand out new ids
+// beta^0 = mu in phi form for the fresh groups: item = (fresh group, edge, half group)
+__global__ void __launch_bounds__(THREADS) rc_seed_kernel(RcState s, const __grid_constant__ QcGrid grid,
+                                                          const float* mu, float* msgs, int E, int gamma) {
+  const int F = *s.fresh_count;
+  const long long items = (long long)F * E * 2;
+  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int h = (int)(it & 1);
+    const long long r = it >> 1;
+    const int e = (int)(r % E);
+    const int g0 = s.fresh_list[r / E] * GROUP + 4 * h;
+    const int m = e / grid.L, l = e - m * grid.L;
+    const int j = m / grid.p, rr = m - j * grid.p;
+    int cc = rr + grid.s[j * grid.L + l];
+    cc -= (cc >= grid.p) ? grid.p : 0;
+    float v[4];
+    vload<4>(mu + (size_t)(l * grid.p + cc) * gamma + g0, v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      v[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(v[i]))) | (__float_as_uint(v[i]) & 0x80000000u));
+    vstore<4>(msgs + (size_t)e * gamma + g0, v);
+  }
+}
+
+// finish: count frozen / capped codewords, freeze them, restart finished groups
 __global__ void rc_finish_kernel(RcState s, RcConfig c) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = g < c.gamma;
   const int64_t k = valid ? s.slot_cw[g] : -1;
-  bool start = false;
-  if (k >= 0) {
+  const bool was_active = valid && ((s.active[g >> 5] >> (g & 31)) & 1u);
+  bool still = false;
+  if (was_active) {
     const int it = s.slot_it[g] + 1;
+    s.slot_it[g] = it;
     const bool ok = !((s.bad[g >> 5] >> (g & 31)) & 1u);
     if (ok || it >= c.max_it) {
       const int64_t b = (k / c.gref) * c.world + c.rank;
@@ -141,70 +152,66 @@ __global__ void rc_finish_kernel(RcState s, RcConfig c) {
         atomicAdd((unsigned long long*)&s.counts[b * 3 + 1], (unsigned long long)bits);
         atomicAdd((unsigned long long*)&s.counts[b * 3 + 2], bits > 0 ? 1ull : 0ull);
       }
-      const int64_t nk = (int64_t)atomicAdd((unsigned long long*)s.next_id, 1ull);
-      if (nk < c.id_limit) {
-        s.slot_cw[g] = nk;
-        s.slot_it[g] = 0;
-        start = true;
-      } else {
-        s.slot_cw[g] = -1;
-      }
     } else {
-      s.slot_it[g] = it;
+      still = true;
     }
   }
-  // rebuild the 32-lane words (one warp = one word: gamma % 32 == 0)
-  const unsigned fw = __ballot_sync(0xffffffffu, start);
-  const unsigned aw = __ballot_sync(0xffffffffu, valid && s.slot_cw[valid ? g : 0] >= 0);
-  if (valid && (g & 31) == 0) {
-    s.fresh[g >> 5] = fw;
-    s.active[g >> 5] = aw;
+  // a group restarts when none of its lanes is still iterating
+  unsigned act = __ballot_sync(0xffffffffu, still);
+  const int lane = g & 31, gl = lane & ~(GROUP - 1);
+  const bool group_idle = ((act >> gl) & 0xffu) == 0;
+  bool start = false;
+  int64_t ng = 0;
+  if (valid && group_idle && (g % GROUP) == 0) ng = (int64_t)atomicAdd((unsigned long long*)s.next_group, 1ull);
+  ng = __shfl_sync(0xffffffffu, ng, gl);          // the group leader's new group id
+  if (valid && group_idle) {
+    const int64_t nk = ng * GROUP + (g % GROUP);
+    start = nk < c.id_limit;
+    s.slot_cw[g] = start ? nk : -1;
+    s.slot_it[g] = 0;
+    if (start && (g % GROUP) == 0) s.fresh_list[atomicAdd(s.fresh_count, 1)] = g / GROUP;
+  }
+  act = __ballot_sync(0xffffffffu, still || start);
+  if (valid && lane == 0) {
+    s.active[g >> 5] = act;
     s.bad[g >> 5] = 0;
   }
 }
 
-int launch_rc_cnu(const qc_plan* p, const CnuArgs& a, const QcGrid& g, const uint32_t* fresh, cudaStream_t st) {
-  if (!p->qc_regular || p->check_regular != 24) return fail_arg("lane recycling needs a regular (J, 24) QC grid");
-  if (a.gamma % 64) return fail_arg("lane recycling needs gamma % 64 == 0");
-  const long long n = (long long)p->M * (a.gamma / 2);
-  rc_cnu_kernel<24, 2><<<blocks_for(n), THREADS, 0, st>>>(a, g, fresh);
-  return check_launch("rc_cnu");
-}
+__global__ void rc_reset_fresh_kernel(int32_t* fresh_count) { *fresh_count = 0; }
 
 }  // namespace
-
-int launch_vnu(const qc_plan* p, VnuArgs a, int mode, cudaStream_t s);
-int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s);
-int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s);
-
 }  // namespace qcb
 
 using namespace qcb;
 
-extern "C" {
-
-size_t qc_rc_state_bytes(int gamma) {
-  const size_t W = (size_t)(gamma > 0 ? gamma : 0) / 32;
-  return gamma * 8 + gamma * 4 + 3 * W * 4 + gamma * 4 + 8 + 64;
-}
-
-static RcState rc_state(void* base, int gamma) {
+namespace {
+RcState rc_state(void* base, int gamma) {
   const size_t W = (size_t)gamma / 32;
   char* p = static_cast<char*>(base);
   RcState s;
   s.slot_cw = reinterpret_cast<int64_t*>(p); p += (size_t)gamma * 8;
-  s.next_id = reinterpret_cast<int64_t*>(p); p += 8;
+  s.next_group = reinterpret_cast<int64_t*>(p); p += 8;
   s.slot_it = reinterpret_cast<int32_t*>(p); p += (size_t)gamma * 4;
   s.lane_bits = reinterpret_cast<int32_t*>(p); p += (size_t)gamma * 4;
-  s.fresh = reinterpret_cast<uint32_t*>(p); p += W * 4;
+  s.fresh_list = reinterpret_cast<int32_t*>(p); p += (size_t)(gamma / GROUP) * 4;
+  s.fresh_count = reinterpret_cast<int32_t*>(p); p += 8;
   s.active = reinterpret_cast<uint32_t*>(p); p += W * 4;
   s.bad = reinterpret_cast<uint32_t*>(p);
   s.counts = nullptr;
   return s;
 }
+}  // namespace
+
+extern "C" {
+
+size_t qc_rc_state_bytes(int gamma) {
+  const size_t G = (size_t)(gamma > 0 ? gamma : 0);
+  return G * 8 + 8 + G * 4 + G * 4 + (G / GROUP) * 4 + 8 + 2 * (G / 32) * 4 + 64;
+}
 
 int qc_rc_init(int gamma, int64_t id_limit, void* state, void* stream) {
-  if (gamma <= 0 || gamma % 64 || !state) return fail_arg("bad recycling state arguments");
+  if (gamma <= 0 || gamma % 128 || !state) return fail_arg("bad recycling state arguments");
   RcState s = rc_state(state, gamma);
   RcConfig c{};
   c.gamma = gamma;
@@ -217,19 +224,29 @@ int qc_rc_ticks(const qc_plan* p, int gamma, int gamma_ref, int world, int rank,
                 int64_t n_batches, uint64_t seed_lo, uint64_t seed_hi, uint64_t lane_base, double sigma, int ticks,
                 float* mu, float* msgs, uint32_t* hb, void* state, int64_t* counts, void* stream) {
   if (!p || !mu || !msgs || !hb || !state || !counts) return fail_arg("null argument");
-  if (gamma <= 0 || gamma % 64 || gamma_ref <= 0 || world < 1 || rank < 0 || rank >= world || max_it < 1 || ticks < 0)
+  if (gamma <= 0 || gamma % 128 || gamma_ref <= 0 || world < 1 || rank < 0 || rank >= world || max_it < 1 ||
+      ticks < 0)
     return fail_arg("bad recycling arguments");
+  if (!p->qc_regular) return fail_arg("lane recycling needs an all-live QC grid");
   cudaStream_t st = as_stream(stream);
   RcState s = rc_state(state, gamma);
   s.counts = counts;
   RcConfig c{gamma, gamma_ref, world, rank, max_it, id_limit, n_batches, seed_lo, seed_hi, lane_base, sigma};
   const QcGrid g = make_grid(p);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const unsigned persist = (unsigned)nsm * 8;
   int rc;
   for (int t = 0; t < ticks; ++t) {
-    const long long nch = (long long)((p->N + 3) / 4) * gamma;
-    rc_channel_kernel<<<blocks_for(nch), THREADS, 0, st>>>(s, c, mu, p->N);
+    rc_channel_kernel<<<persist, THREADS, 0, st>>>(s, c, mu, p->N);
+    rc_seed_kernel<<<persist, THREADS, 0, st>>>(s, g, mu, msgs, p->E, gamma);
+    rc_reset_fresh_kernel<<<1, 1, 0, st>>>(s.fresh_count);
     CnuArgs a{msgs, mu, p->d_check_ptr, p->d_edge_var, s.active, nullptr, p->M, gamma};
-    if ((rc = launch_rc_cnu(p, a, g, s.fresh, st))) return rc;
+    if ((rc = launch_cnu_public(p, a, CNU_PHI, st))) return rc;
     VnuArgs v{};
     v.msgs = msgs; v.mu = mu; v.hb = hb; v.active = s.active; v.gamma = gamma;
     if ((rc = launch_vnu(p, v, VNU_PHI, st))) return rc;
@@ -240,11 +257,11 @@ int qc_rc_ticks(const qc_plan* p, int gamma, int gamma_ref, int world, int rank,
   return check_launch("qc_rc_ticks");
 }
 
-/* host-readable progress: next_id (int64) */
+/* host-readable progress: next group id (int64) */
 int qc_rc_next_id(int gamma, const void* state, int64_t* next_id_dev_out, void* stream) {
   if (!state || !next_id_dev_out) return fail_arg("null argument");
   const RcState s = rc_state(const_cast<void*>(state), gamma);
-  cudaMemcpyAsync(next_id_dev_out, s.next_id, 8, cudaMemcpyDeviceToDevice, as_stream(stream));
+  cudaMemcpyAsync(next_id_dev_out, s.next_group, 8, cudaMemcpyDeviceToDevice, as_stream(stream));
   return check_launch("qc_rc_next_id");
 }
 

@@ -217,7 +217,8 @@ class RecycleCampaign:
 
     @staticmethod
     def supports(layout: EdgeLayout) -> bool:
-        return layout.qc is not None and bool((layout.qc.shifts >= 0).all()) and layout.check_regular == 24
+        """All-live QC grids (kernels address edges by shift arithmetic)."""
+        return layout.qc is not None and bool((layout.qc.shifts >= 0).all())
 
     def _ticks(self, sigma, lane_base, id_limit, n_batches, counts):
         _lib.call("qc_rc_ticks", self.plan.handle, self.gk, self.gref, self.W, self.rank, self.iters,
@@ -316,7 +317,7 @@ def _run_block_recycled(layout, config, gamma_kernel, rank, W, g):
     import torch
     rate = 1.0 - layout.n_checks / layout.n_vars
     info_bits = layout.n_vars - layout.n_checks
-    gk = max(64, (gamma_kernel or 4096) // 64 * 64)
+    gk = max(128, (gamma_kernel or 4096) // 128 * 128)
     eng = RecycleCampaign(layout, config.gamma, gk, config.iterations, config.seed, rank, W)
     results = []
     for pi, db in enumerate(config.points()):
