@@ -35,7 +35,12 @@ def _rank(rank, world, port, out):
     cfg2 = q.SimulationConfig(code_id="toy", ebn0_db=[2.0], iterations=8, processors=2, gamma=8,
                               stop_block_errors=10, max_frames=500, seed=5, stream_segment_frames=6)
     res2 = q.run_stream_simulation(code, cfg2, gamma_kernel=32)
-    out[rank] = ([r.row()[:10] for r in res], [r.row()[:10] for r in res2])
+    # early-stop campaign through lane recycling, batches round-robin over ranks
+    lay3 = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(4, 24, 29)))
+    cfg3 = q.SimulationConfig(code_id="es", ebn0_db=[2.6], iterations=20, gamma=32, stop_block_errors=9,
+                              max_frames=4000, seed=2, early_stop=True)
+    res3 = q.run_block_simulation(lay3, cfg3, gamma_kernel=256)
+    out[rank] = ([r.row()[:10] for r in res], [r.row()[:10] for r in res2], [r.row()[:8] for r in res3])
     dist.destroy_process_group()
 
 
@@ -49,3 +54,7 @@ def test_two_ranks_share_counters():
     assert out[0] == out[1]
     assert out[0][0] == camp["toy_block"]
     assert out[0][1] == camp["toy_stream"]
+    from oracle import campaign, qc as oqc
+    want = campaign.block_point(oqc.qc_layout(oqc.array_code_shifts(4, 24, 29), 29), 2.6, 0, iters=20,
+                                gamma=32, seed=2, stop=9, max_frames=4000, early_stop=True)
+    assert tuple(out[0][2][0][5:8]) == want
