@@ -85,10 +85,10 @@ int cnu_pipe_mode() {
   return v;
 }
 
-// returns 1 if launched, 0 if the shape is not supported (caller falls back)
-int launch_cnu_phi_pipe(const qc_plan* p, const CnuArgs& a, cudaStream_t s) {
-  constexpr int DC = 24, VEC = 2;
-  if (p->check_regular != DC || a.active || a.gamma % (THREADS * VEC)) return 0;
+template <int VEC, int CTAS>
+int launch_pipe_v(const qc_plan* p, const CnuArgs& a, cudaStream_t s) {
+  constexpr int DC = 24;
+  if (a.gamma % (THREADS * VEC)) return 0;
   static int nsm = 0;
   static bool attr = false;
   const size_t smem = 2ull * DC * THREADS * VEC * sizeof(float);
@@ -101,9 +101,17 @@ int launch_cnu_phi_pipe(const qc_plan* p, const CnuArgs& a, cudaStream_t s) {
   }
   const int tpc = a.gamma / (THREADS * VEC);
   const int ntiles = p->M * tpc;
-  const int grid = std::min(ntiles, nsm * 2);
+  const int grid = std::min(ntiles, nsm * CTAS);
   cnu_phi_pipe_kernel<DC, VEC><<<grid, THREADS, smem, s>>>(a, ntiles, tpc);
   return 1;
+}
+
+// returns 1 if launched, 0 if the shape is not supported (caller falls back)
+// QCB_CNU_PIPE=1: float2 lanes, 96 KB smem, 2 CTAs/SM; =2: 1 lane, 48 KB, 4 CTAs/SM
+int launch_cnu_phi_pipe(const qc_plan* p, const CnuArgs& a, cudaStream_t s) {
+  if (p->check_regular != 24 || a.active) return 0;
+  if (cnu_pipe_mode() == 2) return launch_pipe_v<1, 4>(p, a, s);
+  return launch_pipe_v<2, 2>(p, a, s);
 }
 
 }  // namespace qcb

@@ -211,9 +211,7 @@ class RecycleCampaign:
         self.hb = torch.zeros((N, self.gk // 32), dtype=torch.int32, device=dev)
         nbytes = int(_lib.load().qc_rc_state_bytes(self.gk))
         self.state = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
-        self.next_id = torch.zeros(1, dtype=torch.int64, device=dev)
         self._graph = None
-        self._key = None
 
     @staticmethod
     def supports(layout: EdgeLayout) -> bool:
@@ -225,8 +223,6 @@ class RecycleCampaign:
                   int(id_limit), int(n_batches), self.k0, self.k1, int(lane_base), float(sigma), self.TICKS,
                   self.mu.data_ptr(), self.msgs.data_ptr(), self.hb.data_ptr(), self.state.data_ptr(),
                   counts.data_ptr(), _lib.stream_handle())
-        _lib.call("qc_rc_next_id", self.gk, self.state.data_ptr(), self.next_id.data_ptr(),
-                  _lib.stream_handle())
 
     def run_point(self, sigma: float, lane_base: int, stop: int, max_frames: int, group=None):
         """Decode until the ordered stop rule is met; returns (frames, bit_errors, frame_errors)."""
@@ -237,7 +233,6 @@ class RecycleCampaign:
         id_limit = max(0, min(local_batches, -(-(n_batches - self.rank) // W))) * gref
         counts = torch.zeros((n_batches + W, 3), dtype=torch.int64, device=self.mu.device)
         _lib.call("qc_rc_init", self.gk, int(id_limit), self.state.data_ptr(), _lib.stream_handle())
-        key = (sigma, lane_base, id_limit, n_batches, counts.data_ptr())
         self._graph = None
         tot, done, scan = (0, 0, 0), False, 0
         # only a window of batches after the consumed prefix can be in flight
@@ -248,7 +243,7 @@ class RecycleCampaign:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     self._ticks(sigma, lane_base, id_limit, n_batches, counts)
-                self._graph, self._key = g, key
+                self._graph = g
             else:
                 self._graph.replay()
             end = min(n_batches, scan + win)

@@ -103,3 +103,43 @@ def test_stream_api_contract(gpu):
         q.StreamDecoder(code, 2, gamma=2).push_frame(np.ones((2, code.c + 1)), 0.8)
     with pytest.raises(ValueError):
         q.unwrap_qc(q.multiplicative_shifts(3, 5, 7))
+
+
+def test_device_slot_counter_matches_host_slots(gpu):
+    """cc_slot with a device-resident slot counter (t_dev + cc_advance, the form a
+    captured CUDA graph replays) is bit-identical to host-indexed slots."""
+    import torch
+    from paper_1204_0334_b200 import _lib
+    q = gpu
+    code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 8))
+    plan = code.plan()
+    I, G, K = 2, 32, 14
+    window = I * (code.ms + 1)
+    rng = np.random.default_rng(5)
+    frames = torch.from_numpy(rng.normal(2.0, 3.0, size=(K, code.c, G)).astype(np.float32)).cuda()
+    outs = []
+    for mode in ("host", "device"):
+        msg = torch.zeros((I * code.edge_count, G), dtype=torch.float32, device="cuda")
+        ring = torch.zeros((window, code.c, G), dtype=torch.float32, device="cuda")
+        post = torch.zeros((K, code.c, G), dtype=torch.float32, device="cuda")
+        cnt = torch.zeros((3, G), dtype=torch.int32, device="cuda")
+        tdev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        s = _lib.stream_handle()
+        for t in range(K):
+            emit = post[t].data_ptr() if t >= window - 1 else None
+            if mode == "host":
+                _lib.call("cc_slot", plan.handle, I, G, t, None, msg.data_ptr(), ring.data_ptr(),
+                          frames[t].data_ptr(), emit, cnt.data_ptr(), s)
+            else:
+                _lib.call("cc_slot", plan.handle, I, G, 0, tdev.data_ptr(), msg.data_ptr(), ring.data_ptr(),
+                          frames[t].data_ptr(), emit, cnt.data_ptr(), s)
+                _lib.call("cc_advance", tdev.data_ptr(), 1, s)
+        _lib.call("cc_fold", cnt.data_ptr(), G, s)
+        torch.cuda.synchronize()
+        if mode == "device":
+            assert int(tdev.item()) == K
+        outs.append((msg.cpu().numpy(), post.cpu().numpy(), cnt.cpu().numpy()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    # one emitted frame per slot from window-1 on, counters folded per frame
+    assert int(outs[0][2][1].sum()) == int((outs[0][1][window - 1:] < 0).sum())
