@@ -11,8 +11,10 @@ The message store (E x gamma fp32 = 294 KB x gamma) exceeds the 126 MB L2 for
 gamma >= 512, so consecutive steps cannot be served from L2 (no flush needed).
 
 `e2e` = the same metric through the public API (`decode_batch`) with host
-numpy inputs: each step copies y (gamma x N fp64, pinned) host->device and
-reads posteriors (fp64) + hard bits (u8) + syndrome flags back.
+numpy inputs: each step copies y (gamma x N fp64, page-locked) host->device and
+reads posteriors (fp64) + hard bits (u8) + syndrome flags + iteration counts
+back (native chunked pipeline, csrc/host_pipe.cu); `pageable_input_value` is
+the same with y in ordinary pageable memory.
 
 `roofline` = the check-node kernel (the dominant launch): algorithmic bytes per
 launch (read + write of E x gamma fp32 packages) / its CUDA-event-timed
@@ -330,26 +332,41 @@ def main():
                          "frac": round(step_alg / (ms / args.steps / 1e3) / 1e9 / peak, 4)}}
 
     # ---- e2e through the public API with host buffers ----
+    # decode_batch(layout, y, sigma, 30) with y (gamma, N) fp64 in page-locked
+    # host memory (the contract's "inputs from pinned host memory"); every step
+    # copies y in and reads posteriors (fp64) + hard bits (u8) + syndrome flags
+    # + iteration counts back; the result arrays come from the caching pinned
+    # allocator and are dropped each step like a user's loop would.
     e2e = None
     if not args.no_e2e:
-        from oracle import channel as och  # input generation only (host data), not measured
         import numpy as np
         rng = np.random.default_rng(rank)
-        y = 1.0 + sigma * rng.standard_normal((gamma, N))
-        for _ in range(2):
-            q.decode_batch(lay, y, sigma, ITERS)
-        barrier()
-        t0 = time.perf_counter()
-        e_steps = max(3, args.steps // 4)
-        for _ in range(e_steps):
-            r = q.decode_batch(lay, y, sigma, ITERS)
-        barrier()
-        dt = max_scalar(time.perf_counter() - t0, group, device="cuda")
-        e2e = {"value": round(e_steps * gamma * W * K_info / dt / 1e6, 2), "unit": "Mbit/s",
+        y_pageable = 1.0 + sigma * rng.standard_normal((gamma, N))
+        y = q.host_array(y_pageable)
+
+        def e2e_rate(yin, steps):
+            r = None
+            for _ in range(2):
+                r = q.decode_batch(lay, yin, sigma, ITERS)
+            del r
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                r = q.decode_batch(lay, yin, sigma, ITERS)
+                del r
+            barrier()
+            dt = max_scalar(time.perf_counter() - t0, group, device="cuda")
+            return round(steps * gamma * W * K_info / dt / 1e6, 2)
+
+        e_steps = max(3, args.steps // 2)
+        e2e = {"value": e2e_rate(y, e_steps), "unit": "Mbit/s",
                "h2d_bytes_per_step": gamma * N * 8,
-               "d2h_bytes_per_step": gamma * N * 4 + gamma * N + 2 * gamma * 4,
-               "api": "paper_1204_0334_b200.decode_batch (numpy in, DecodeResult out)"}
-        del och
+               "d2h_bytes_per_step": gamma * N * 8 + gamma * N + gamma + gamma * 4,
+               "api": "paper_1204_0334_b200.decode_batch (numpy y in page-locked host memory; "
+                      "DecodeResult out: fp64 posteriors, u8 bits, ok, iterations)",
+               "steps": e_steps,
+               "pageable_input_value": e2e_rate(y_pageable, max(2, e_steps // 2))}
+        del y, y_pageable
 
     stream = stream_bench(args, q, rank, W, group, barrier) if args.stream_gamma else None
 

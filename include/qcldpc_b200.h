@@ -110,6 +110,26 @@ QC_API int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post,
 QC_API int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma,
                                   float* mu_vm, void* stream);
 
+/* ---- host-buffer decode (decode_batch / decode_llr_batch, bp.py:213-274) ---
+ * The reference's public decode with caller-owned HOST arrays: x (gamma, N)
+ * fp64 lane-major received values (sigma > 0) or LLRs (sigma <= 0); outputs
+ * bits (gamma, N) u8, post (gamma, N) fp64, ok (gamma) u8 (syndrome_ok),
+ * iters_run (gamma) i64 -- DecodeResult (bp.py:87-100); bits/post/ok/iters_run
+ * may each be NULL.  Chunks of `chunk` lanes rotate over `slots` CUDA streams
+ * (copy-in, graph-replayed decode and copy-out overlap); page-locked host
+ * arrays are DMA'd in place, pageable ones staged.  The call returns when the
+ * outputs are in host memory.  A qc_host_dec is bound to the device current
+ * at creation, keeps a pointer to `plan` (which must outlive it) and is not
+ * thread-safe (one caller at a time). */
+typedef struct qc_host_dec qc_host_dec;
+QC_API int qc_host_create(const qc_plan* plan, int chunk, int slots, int iters, int early_stop,
+                          qc_host_dec** out);
+QC_API void qc_host_destroy(qc_host_dec* dec);
+/* dims: chunk, slots, iters, early_stop, device */
+QC_API int qc_host_dims(const qc_host_dec* dec, int64_t* dims);
+QC_API int qc_host_decode(qc_host_dec* dec, const double* x, int gamma, double sigma, uint8_t* bits,
+                          double* post, uint8_t* ok, int64_t* iters_run);
+
 /* ---- lane-recycling early-stop campaign engine (harness.py:144-204 with
  * early_stop=True): a lane whose codeword froze (bp.py:242-256) or hit the
  * iteration cap immediately starts codeword next_id; per-codeword results and

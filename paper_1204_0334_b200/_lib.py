@@ -42,6 +42,10 @@ SIGNATURES = {
     "qc_lane_major": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_lane_major_f32": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_llr_from_lane_major": (_i, [_i, _i, _i, _p, _d, _p, _p]),
+    "qc_host_create": (_i, [_p, _i, _i, _i, _i, C.POINTER(_p)]),
+    "qc_host_destroy": (None, [_p]),
+    "qc_host_dims": (_i, [_p, _p]),
+    "qc_host_decode": (_i, [_p, _p, _i, _d, _p, _p, _p, _p]),
     "qc_rc_state_bytes": (C.c_size_t, [_i]),
     "qc_rc_init": (_i, [_i, _i64, _p, _p]),
     "qc_rc_ticks": (_i, [_p, _i, _i, _i, _i, _i, _i64, _i64, _u64, _u64, _u64, _d, _i, _p, _p, _p, _p, _p, _p]),

@@ -11,9 +11,11 @@ csrc/phi.cuh); against the float64 reference a single update agrees to
 |delta| <= 1e-4 * max(|ref|, 1), and decisions / syndromes / error counts of
 full decodes are checked bit-exact by tests/test_gpu_block.py.
 
-`BlockDecoder` is the B200-side engine behind `decode_batch` /
-`decode_llr_batch`: persistent device buffers, the whole flooding loop
-captured once in a CUDA graph and replayed per batch.
+`decode_batch` / `decode_llr_batch` run on `HostDecoder`, the native
+host-buffer pipeline (csrc/host_pipe.cu): lane chunks rotate over CUDA
+streams so PCIe copies overlap the graph-replayed decode, page-locked arrays
+are DMA'd in place.  `BlockDecoder` is the device-resident engine (inputs and
+outputs in HBM) used by the campaign drivers and the float64 build.
 """
 
 from __future__ import annotations
@@ -29,7 +31,7 @@ from .plan import get_precision, lane_words, pad32, require_cuda, unpack_planes
 __all__ = [
     "L_MAX", "TANH_CLAMP", "MessageBatch", "DecodeResult", "channel_llrs", "init_messages",
     "check_node_update", "variable_node_update", "hard_decision_and_syndrome",
-    "decode_llr_batch", "decode_batch", "BlockDecoder",
+    "decode_llr_batch", "decode_batch", "BlockDecoder", "HostDecoder", "host_array",
 ]
 
 L_MAX = 50.0
@@ -314,55 +316,85 @@ class BlockDecoder:
         return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
 
 
-PIPELINE_CHUNK = 1024   # lanes per pipelined chunk of the host-buffer API
+HOST_CHUNK = 256        # lanes per pipelined chunk of the host-buffer API (tools/e2e_bench.py)
+HOST_SLOTS = 4          # CUDA streams (device buffer sets) the chunks rotate over
+PINNED_MIN_BYTES = 1 << 20
 
 
-def _pipelined(layout: EdgeLayout, x: np.ndarray, sigma, iterations: int, early_stop: bool) -> DecodeResult:
-    """Host-buffer decode of a large batch in chunks of PIPELINE_CHUNK lanes on
-    two CUDA streams: while chunk k decodes, chunk k+1 is copied in and chunk
-    k-1 is read back, so the PCIe / host-memory traffic overlaps the kernels."""
+class HostDecoder:
+    """Native host-buffer pipeline (qc_host_* in include/qcldpc_b200.h): chunks of
+    `chunk` lanes rotate over `slots` streams, so the copy-in of chunk k+1 and
+    the copy-out of chunk k-1 overlap the graph-replayed decode of chunk k."""
+
+    def __init__(self, layout: EdgeLayout, chunk: int, slots: int, iterations: int, early_stop: bool):
+        import ctypes
+        require_cuda()
+        self.layout = layout
+        self.plan = layout.plan()          # must outlive the native decoder
+        h = ctypes.c_void_p()
+        _lib.call("qc_host_create", self.plan.handle, chunk, slots, iterations, int(early_stop),
+                  ctypes.byref(h))
+        self.handle = h.value
+        self.chunk, self.slots = chunk, slots
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h and _lib._LIB is not None:
+            _lib.load().qc_host_destroy(h)
+
+    def decode(self, x: np.ndarray, sigma: float) -> DecodeResult:
+        """x (gamma, N) fp64: received values (sigma > 0) or LLRs (sigma = 0)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        G, n = x.shape
+        post = host_empty((G, n), np.float64)
+        bits = host_empty((G, n), np.uint8)
+        ok = np.empty(G, dtype=bool)
+        its = np.empty(G, dtype=np.int64)
+        _lib.call("qc_host_decode", self.handle, x.ctypes.data, G, float(sigma), bits.ctypes.data,
+                  post.ctypes.data, ok.ctypes.data, its.ctypes.data)
+        return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """Output array for the host-buffer API: large ones come from torch's caching
+    page-locked allocator, so the decoder DMAs straight into them and a freed
+    result's pages are reused by the next call (no fresh page faults)."""
+    dtype = np.dtype(dtype)
+    if int(np.prod(shape)) * dtype.itemsize < PINNED_MIN_BYTES:
+        return np.empty(shape, dtype=dtype)
     import torch
-    G, n = x.shape
-    post = np.empty((G, n), dtype=np.float64)
-    bits = np.empty((G, n), dtype=np.uint8)
-    ok = np.empty(G, dtype=bool)
-    its = np.empty(G, dtype=np.int64)
-    decs = [_decoder(layout, PIPELINE_CHUNK, iterations, early_stop, slot=i) for i in (0, 1)]
-    cache = layout.__dict__.setdefault("_streams", [])
-    while len(cache) < 2:
-        cache.append(torch.cuda.Stream())
-    streams = cache[:2]
-    cur = torch.cuda.current_stream()
-    for st in streams:
-        st.wait_stream(cur)
-    pending = [None, None]
-    starts = list(range(0, G, PIPELINE_CHUNK))
-    for k, a in enumerate(starts):
-        b = min(G, a + PIPELINE_CHUNK)
-        i = k % 2
-        if pending[i] is not None:
-            pa, pb = pending[i]
-            decs[i].collect_result(pb - pa, post, bits, ok, its, pa)
-        with torch.cuda.stream(streams[i]):
-            decs[i].load_lane_major(x[a:b], sigma)
-            decs[i].run()
-            decs[i].stage_result(b - a)
-        pending[i] = (a, b)
-    for k in range(len(starts), len(starts) + 2):
-        i = k % 2
-        if pending[i] is not None:
-            pa, pb = pending[i]
-            decs[i].collect_result(pb - pa, post, bits, ok, its, pa)
-            pending[i] = None
-    for st in streams:
-        cur.wait_stream(st)
-    return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
+           np.dtype(np.float32): torch.float32}[dtype]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
 
 
-def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool, slot: int = 0) -> BlockDecoder:
+def host_array(a: np.ndarray) -> np.ndarray:
+    """Copy of `a` in page-locked host memory (inputs the decoder DMAs in place)."""
+    out = host_empty(a.shape, a.dtype)
+    np.copyto(out, a)
+    return out
+
+
+def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool) -> HostDecoder:
+    import torch
+    chunk = min(HOST_CHUNK, pad32(gamma))
+    slots = HOST_SLOTS if gamma > chunk else 1
+    cache = layout.__dict__.setdefault("_host_decoders", {})
+    key = (chunk, slots, iterations, bool(early_stop), torch.cuda.current_device())
+    dec = cache.get(key)
+    if dec is None:
+        if len(cache) >= 6:
+            cache.clear()
+        dec = HostDecoder(layout, chunk, slots, iterations, early_stop)
+        cache[key] = dec
+    return dec
+
+
+def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool) -> BlockDecoder:
+    """float64 conformance build: device engine at the batch's own gamma."""
     cache = layout.__dict__.setdefault("_decoders", {})
     import torch
-    key = (pad32(gamma), iterations, bool(early_stop), slot, get_precision(), torch.cuda.current_device())
+    key = (pad32(gamma), iterations, bool(early_stop), get_precision(), torch.cuda.current_device())
     dec = cache.get(key)
     if dec is None:
         if len(cache) >= 8:
@@ -370,6 +402,17 @@ def _decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool, 
         dec = BlockDecoder(layout, pad32(gamma), iterations, early_stop, count_bits=False)
         cache[key] = dec
     return dec
+
+
+def _decode_host(layout: EdgeLayout, x: np.ndarray, sigma: float | None, iterations: int,
+                 early_stop: bool) -> DecodeResult:
+    require_cuda()
+    if get_precision() == "float64":
+        dec = _decoder(layout, x.shape[0], iterations, early_stop)
+        dec.load_lane_major(x, sigma)
+        dec.run()
+        return dec.result(x.shape[0])
+    return _host_decoder(layout, x.shape[0], iterations, early_stop).decode(x, sigma or 0.0)
 
 
 def decode_llr_batch(layout: EdgeLayout, mu: np.ndarray, iterations: int,
@@ -380,12 +423,7 @@ def decode_llr_batch(layout: EdgeLayout, mu: np.ndarray, iterations: int,
     mu = np.atleast_2d(np.asarray(mu, dtype=np.float64))
     if mu.shape[1] != layout.n_vars:
         raise ValueError(f"mu has {mu.shape[1]} symbols, layout has {layout.n_vars}")
-    if mu.shape[0] > 2 * PIPELINE_CHUNK:
-        return _pipelined(layout, mu, None, iterations, early_stop)
-    dec = _decoder(layout, mu.shape[0], iterations, early_stop)
-    dec.load_lane_major(mu, None)
-    dec.run()
-    return dec.result(mu.shape[0])
+    return _decode_host(layout, mu, None, iterations, early_stop)
 
 
 def decode_batch(layout: EdgeLayout, y: np.ndarray, sigma: float, iterations: int,
@@ -398,9 +436,4 @@ def decode_batch(layout: EdgeLayout, y: np.ndarray, sigma: float, iterations: in
         raise ValueError("need at least one iteration")
     s = abs(float(sigma))
     s = s if s > 0.0 else 1e-300
-    if y.shape[0] > 2 * PIPELINE_CHUNK:
-        return _pipelined(layout, y, s, iterations, early_stop)
-    dec = _decoder(layout, y.shape[0], iterations, early_stop)
-    dec.load_lane_major(y, s)
-    dec.run()
-    return dec.result(y.shape[0])
+    return _decode_host(layout, y, s, iterations, early_stop)

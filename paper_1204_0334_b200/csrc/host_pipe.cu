@@ -1,0 +1,317 @@
+// Host-buffer decode pipeline: the reference's decode_batch / decode_llr_batch
+// (/root/reference/pkg/src/qcldpc/bp.py:213-274) with caller-owned HOST arrays,
+// lane-major in and out exactly as DecodeResult (bp.py:87-100).
+//
+// A batch of gamma codewords is cut into chunks of `chunk` lanes that rotate
+// over `slots` CUDA streams, each with its own device buffers and an
+// instantiated CUDA graph of the whole flooding loop (qc_decode).  Per chunk:
+//   H2D of the received values (fp64, lane-major)
+//   -> LLR scale/clip/transpose kernel -> graph (init + iters x (check, variable)
+//      + hard decision + syndrome) -> lane-major fp64 posteriors + u8 bits
+//   -> D2H of posteriors, bits, syndrome flags, iteration counts.
+// While one chunk decodes, the next is copied in and the previous one is read
+// back, so PCIe (55 GB/s each way on the B200 box, profiles/r02/pcie.json)
+// overlaps the kernels.  Host arrays that are page-locked (cudaHostAlloc /
+// torch pin_memory / cudaHostRegister) are DMA'd in place; pageable arrays go
+// through per-slot pinned staging with a multi-threaded memcpy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "plan.h"
+
+namespace {
+
+using namespace qcb;
+
+struct Slot {
+  cudaStream_t st = nullptr;
+  cudaEvent_t done = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  double* x = nullptr;          // (chunk, N) fp64 lane-major input
+  float* mu = nullptr;          // (N, chunk) fp32 LLRs
+  float* msgs = nullptr;        // (E, chunk) packages
+  float* post = nullptr;        // (N, chunk) fp32 posteriors
+  uint32_t* hb = nullptr;       // (N, chunk/32) hard-bit planes
+  uint32_t* work = nullptr;     // qc_decode scratch
+  uint8_t* ok = nullptr;        // (chunk)
+  int32_t* its = nullptr;       // (chunk)
+  double* post_lm = nullptr;    // (chunk, N) fp64 lane-major posteriors
+  uint8_t* bits_lm = nullptr;   // (chunk, N) u8 lane-major hard bits
+  // page-locked staging (allocated on first use with a pageable array)
+  double* h_in = nullptr;
+  double* h_post = nullptr;
+  uint8_t* h_bits = nullptr;
+  uint8_t* h_ok = nullptr;      // always used (small)
+  int32_t* h_its = nullptr;
+  // chunk in flight: lanes [a, b) of the current call, or a < 0
+  long long a = -1, b = -1;
+};
+
+void par_copy(void* dst, const void* src, size_t bytes) {
+  const size_t MIN_PER_THREAD = size_t(8) << 20;
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  size_t T = std::min<size_t>({hw, 16, std::max<size_t>(1, bytes / MIN_PER_THREAD)});
+  if (T <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  size_t per = (bytes + T - 1) / T;
+  per = (per + 4095) & ~size_t(4095);
+  for (size_t t = 0; t < T; ++t) {
+    size_t lo = t * per;
+    if (lo >= bytes) break;
+    size_t n = std::min(per, bytes - lo);
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, n); });
+  }
+  for (auto& t : th) t.join();
+}
+
+bool pinned_one(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// page-locked iff both ends are (a view into one pinned allocation)
+bool pinned(const void* p, size_t bytes) {
+  if (!p || bytes == 0) return false;
+  return pinned_one(p) && pinned_one(static_cast<const char*>(p) + bytes - 1);
+}
+
+#define HP_CK(expr)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess) return fail_rt(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct qc_host_dec {
+  const qc_plan* plan = nullptr;
+  int chunk = 0, iters = 0, early_stop = 0, device = 0;
+  std::vector<Slot> slots;
+};
+
+static void free_slot(Slot& s) {
+  if (s.graph) cudaGraphExecDestroy(s.graph);
+  if (s.done) cudaEventDestroy(s.done);
+  if (s.st) cudaStreamDestroy(s.st);
+  void* dev[] = {s.x, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, s.post_lm, s.bits_lm};
+  for (void* d : dev)
+    if (d) cudaFree(d);
+  void* host[] = {s.h_in, s.h_post, s.h_bits, s.h_ok, s.h_its};
+  for (void* h : host)
+    if (h) cudaFreeHost(h);
+  s = Slot{};
+}
+
+static int init_slot(qc_host_dec* h, Slot& s) {
+  const qc_plan* p = h->plan;
+  const size_t C = h->chunk, N = p->N, E = std::max(p->E, 1);
+  HP_CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+  HP_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  HP_CK(cudaMalloc(&s.x, C * N * sizeof(double)));
+  HP_CK(cudaMalloc(&s.mu, N * C * sizeof(float)));
+  HP_CK(cudaMalloc(&s.msgs, E * C * sizeof(float)));
+  HP_CK(cudaMalloc(&s.post, N * C * sizeof(float)));
+  HP_CK(cudaMalloc(&s.hb, N * (C / 32) * sizeof(uint32_t)));
+  HP_CK(cudaMalloc(&s.work, qc_decode_work_words(h->chunk) * sizeof(uint32_t)));
+  HP_CK(cudaMalloc(&s.ok, C));
+  HP_CK(cudaMalloc(&s.its, C * sizeof(int32_t)));
+  HP_CK(cudaMalloc(&s.post_lm, C * N * sizeof(double)));
+  HP_CK(cudaMalloc(&s.bits_lm, C * N));
+  HP_CK(cudaMallocHost(&s.h_ok, C));
+  HP_CK(cudaMallocHost(&s.h_its, C * sizeof(int32_t)));
+  HP_CK(cudaMemsetAsync(s.msgs, 0, E * C * sizeof(float), s.st));
+  // the flooding loop, captured once: replayed per chunk
+  cudaGraph_t g = nullptr;
+  HP_CK(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
+  int rc = qc_decode(p, h->chunk, h->iters, h->early_stop, s.mu, s.msgs, s.post, s.hb, s.work, s.ok,
+                     s.its, nullptr, s.st);
+  cudaError_t ce = cudaStreamEndCapture(s.st, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess) return fail_rt(std::string("graph capture: ") + cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&s.graph, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail_rt(std::string("graph instantiate: ") + cudaGetErrorString(ce));
+  HP_CK(cudaStreamSynchronize(s.st));
+  return 0;
+}
+
+extern "C" {
+
+int qc_host_create(const qc_plan* plan, int chunk, int slots, int iters, int early_stop, qc_host_dec** out) {
+  if (!plan || !out) return fail_arg("null argument");
+  if (chunk <= 0 || chunk % 32) return fail_arg("chunk must be a positive multiple of 32");
+  if (slots < 1 || slots > 8) return fail_arg("slots must be in [1, 8]");
+  if (iters < 1) return fail_arg("need at least one iteration");
+  *out = nullptr;
+  auto* h = new qc_host_dec();
+  h->plan = plan;
+  h->chunk = chunk;
+  h->iters = iters;
+  h->early_stop = early_stop ? 1 : 0;
+  if (cudaGetDevice(&h->device) != cudaSuccess) {
+    delete h;
+    return fail_rt("no CUDA device");
+  }
+  h->slots.resize(slots);
+  for (auto& s : h->slots) {
+    if (int rc = init_slot(h, s)) {
+      for (auto& t : h->slots) free_slot(t);
+      delete h;
+      return rc;
+    }
+  }
+  *out = h;
+  return 0;
+}
+
+void qc_host_destroy(qc_host_dec* h) {
+  if (!h) return;
+  DeviceGuard g(h->device);
+  for (auto& s : h->slots) {
+    if (s.st) cudaStreamSynchronize(s.st);
+    free_slot(s);
+  }
+  delete h;
+}
+
+int qc_host_dims(const qc_host_dec* h, int64_t* dims) {
+  if (!h || !dims) return fail_arg("null argument");
+  dims[0] = h->chunk;
+  dims[1] = (int64_t)h->slots.size();
+  dims[2] = h->iters;
+  dims[3] = h->early_stop;
+  dims[4] = h->device;
+  return 0;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct Call {
+  qc_host_dec* h;
+  int N;
+  double* post;
+  uint8_t* bits;
+  uint8_t* ok;
+  int64_t* its;
+  bool pin_post, pin_bits;
+};
+
+// wait for the slot's chunk and move its results into the caller's arrays
+int finish(const Call& c, Slot& s) {
+  if (s.a < 0) return 0;
+  HP_CK(cudaEventSynchronize(s.done));
+  const size_t n = (size_t)(s.b - s.a) * c.N;
+  if (c.post && !c.pin_post) par_copy(c.post + (size_t)s.a * c.N, s.h_post, n * sizeof(double));
+  if (c.bits && !c.pin_bits) par_copy(c.bits + (size_t)s.a * c.N, s.h_bits, n);
+  for (long long g = s.a; g < s.b; ++g) {
+    if (c.ok) c.ok[g] = s.h_ok[g - s.a] ? 1 : 0;
+    if (c.its) c.its[g] = s.h_its[g - s.a];
+  }
+  s.a = s.b = -1;
+  return 0;
+}
+
+int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits, double* post, uint8_t* ok,
+        int64_t* iters_run) {
+  const qc_plan* p = h->plan;
+  const int N = p->N;
+  const size_t row = (size_t)N;
+  Call c{h, N, post, bits, ok, iters_run, pinned(post, (size_t)gamma * row * sizeof(double)),
+         pinned(bits, (size_t)gamma * row)};
+  const bool pin_in = pinned(x, (size_t)gamma * row * sizeof(double));
+  const int S = (int)h->slots.size();
+  const long long nchunks = (gamma + h->chunk - 1) / h->chunk;
+  const size_t C = h->chunk;
+  for (long long k = 0; k < nchunks; ++k) {
+    Slot& s = h->slots[k % S];
+    if (int rc = finish(c, s)) return rc;
+    const long long a = k * h->chunk, b = std::min<long long>(gamma, a + h->chunk);
+    const int gi = (int)(b - a);
+    const double* src = x + (size_t)a * row;
+    if (!pin_in) {
+      if (!s.h_in) HP_CK(cudaMallocHost(&s.h_in, C * row * sizeof(double)));
+      par_copy(s.h_in, src, (size_t)gi * row * sizeof(double));
+      src = s.h_in;
+    }
+    HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
+    if (int rc = qc_llr_from_lane_major(N, h->chunk, gi, s.x, sigma, s.mu, s.st)) return rc;
+    HP_CK(cudaGraphLaunch(s.graph, s.st));
+    if (int rc = qc_lane_major(N, h->chunk, gi, s.post, post ? s.post_lm : nullptr,
+                               bits ? s.bits_lm : nullptr, s.st))
+      return rc;
+    if (post) {
+      double* dst = c.pin_post ? post + (size_t)a * row : nullptr;
+      if (!dst) {
+        if (!s.h_post) HP_CK(cudaMallocHost(&s.h_post, C * row * sizeof(double)));
+        dst = s.h_post;
+      }
+      HP_CK(cudaMemcpyAsync(dst, s.post_lm, (size_t)gi * row * sizeof(double), cudaMemcpyDeviceToHost, s.st));
+    }
+    if (bits) {
+      uint8_t* dst = c.pin_bits ? bits + (size_t)a * row : nullptr;
+      if (!dst) {
+        if (!s.h_bits) HP_CK(cudaMallocHost(&s.h_bits, C * row));
+        dst = s.h_bits;
+      }
+      HP_CK(cudaMemcpyAsync(dst, s.bits_lm, (size_t)gi * row, cudaMemcpyDeviceToHost, s.st));
+    }
+    HP_CK(cudaMemcpyAsync(s.h_ok, s.ok, gi, cudaMemcpyDeviceToHost, s.st));
+    HP_CK(cudaMemcpyAsync(s.h_its, s.its, gi * sizeof(int32_t), cudaMemcpyDeviceToHost, s.st));
+    HP_CK(cudaEventRecord(s.done, s.st));
+    s.a = a;
+    s.b = b;
+  }
+  for (long long k = std::max<long long>(0, nchunks - S); k < nchunks; ++k)
+    if (int rc = finish(c, h->slots[k % S])) return rc;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int qc_host_decode(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
+                              double* post, uint8_t* ok, int64_t* iters_run) {
+  if (!h) return fail_arg("null decoder");
+  if (gamma < 0) return fail_arg("gamma must be >= 0");
+  if (gamma > 0 && !x) return fail_arg("null input");
+  if (gamma == 0) return 0;
+  DeviceGuard guard(h->device);
+  int rc = run(h, x, gamma, sigma, bits, post, ok, iters_run);
+  if (rc) {                       // leave no chunk in flight for the next call
+    for (auto& s : h->slots) {
+      cudaStreamSynchronize(s.st);
+      s.a = s.b = -1;
+    }
+    cudaGetLastError();
+  }
+  return rc;
+}

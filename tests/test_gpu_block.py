@@ -204,10 +204,11 @@ def test_decode_errors(gpu):
 
 
 def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
-    """decode_batch above 2 x PIPELINE_CHUNK lanes runs chunked on two streams."""
+    """decode_batch above HOST_CHUNK lanes runs chunked over HOST_SLOTS streams
+    (ragged last chunk); pinned and pageable host arrays give identical results."""
     q = gpu
     from paper_1204_0334_b200 import bp as qbp
-    monkeypatch.setattr(qbp, "PIPELINE_CHUNK", 64)
+    monkeypatch.setattr(qbp, "HOST_CHUNK", 64)
     lay = toy(q)
     rng = np.random.default_rng(77)
     y = rng.normal(1.0, 1.0, size=(300, lay.n_vars))
@@ -219,6 +220,32 @@ def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
     close(r.posteriors, post)
     r2 = q.decode_batch(lay, y[:64], 1.0, 12)
     assert np.array_equal(r2.posteriors, r.posteriors[:64])
+    monkeypatch.setattr(qbp, "PINNED_MIN_BYTES", 0)      # page-locked in and out: DMA in place
+    r3 = q.decode_batch(lay, q.host_array(y), 1.0, 12)
+    for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
+        assert np.array_equal(getattr(r3, f), getattr(r, f)), f
+    r4 = q.decode_batch(lay, y, 1.0, 12, early_stop=True)
+    bits, post, ok, its = obp.decode_llr(olay, obp.channel_llrs(y, 1.0), 12, early_stop=True)
+    assert np.array_equal(r4.hard_bits, bits) and np.array_equal(r4.iterations_run, its)
+
+
+def test_host_pipeline_abi(gpu):
+    """qc_host_* through ctypes: argument errors map to ValueError, dims round-trip."""
+    import ctypes
+    q = gpu
+    from paper_1204_0334_b200 import _lib
+    lay = toy(q)
+    h = ctypes.c_void_p()
+    with pytest.raises(ValueError):
+        _lib.call("qc_host_create", lay.plan().handle, 48, 2, 5, 0, ctypes.byref(h))
+    with pytest.raises(ValueError):
+        _lib.call("qc_host_create", lay.plan().handle, 64, 0, 5, 0, ctypes.byref(h))
+    dec = q.HostDecoder(lay, 64, 2, 5, True)
+    dims = np.zeros(5, dtype=np.int64)
+    _lib.call("qc_host_dims", dec.handle, dims.ctypes.data)
+    assert list(dims[:4]) == [64, 2, 5, 1]
+    r = dec.decode(np.zeros((0, lay.n_vars)), 1.0)
+    assert r.hard_bits.shape == (0, lay.n_vars)
 
 
 _PIPE_SNIPPET = r"""
