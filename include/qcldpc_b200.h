@@ -87,13 +87,34 @@ QC_API int qc_bit_errors(const qc_plan* plan, int gamma, const uint32_t* hb, int
 
 /* decode_llr_batch (bp.py:213-265), whole loop on device.
  * mu (N,gamma) clipped LLRs; msgs (E,gamma) scratch; post (N,gamma) out;
- * hb (N,gamma/32) out; work: qc_decode_work_words(gamma) uint32 scratch;
+ * hb (N,gamma/32) out; work: qc_decode_work_words(plan, gamma) uint32 scratch
+ * (for regular QC codes it holds the compact check records, 3 M gamma words);
  * ok (gamma) u8 out; iters_run (gamma) i32 out; lane_bits (gamma) i32 out
  * (may be NULL).  early_stop reproduces bp.py:242-256 (freeze on syndrome). */
-QC_API size_t qc_decode_work_words(int gamma);
+QC_API size_t qc_decode_work_words(const qc_plan* plan, int gamma);
 QC_API int qc_decode(const qc_plan* plan, int gamma, int iters, int early_stop, const float* mu,
               float* msgs, float* post, uint32_t* hb, uint32_t* work, uint8_t* ok,
               int32_t* iters_run, int32_t* lane_bits, void* stream);
+
+/* The two passes of qc_decode's compact check-state schedule (regular QC
+ * plans; bit-identical to qc_cnu_ex mode 2 + qc_vnu_ex mode 1):
+ * qc_agg_check: check records agg (M, 3, gamma) = (S | parity sign bit, S2, max)
+ *   of the phi-form packages (from_mu = 1: of beta^0 = mu, iteration 1);
+ * qc_agg_var: each variable re-derives its check->var messages from agg and the
+ *   package it replaces (flags & 1: iteration 1, packages implied by mu), then
+ *   writes phi-form packages, or (flags & 2: last iteration) post / hb only. */
+QC_API int qc_agg_check(const qc_plan* plan, int gamma, int from_mu, float* msgs, const float* mu,
+                        float* agg, void* stream);
+QC_API int qc_agg_var(const qc_plan* plan, int gamma, int flags, float* msgs, const float* mu,
+                      const float* agg, float* post, uint32_t* hb, void* stream);
+/* One launch of both: qc_agg_var on lanes [var_lane0, +lanes) and qc_agg_check
+ * on lanes [check_lane0, +lanes) (disjoint windows, 128-lane aligned, gamma %
+ * 256 == 0; the decode loop's half-iteration step). */
+QC_API int qc_agg_fused(const qc_plan* plan, int gamma, int lanes, int var_lane0, int var_flags,
+                        int check_lane0, int check_from_mu, float* msgs, const float* mu, float* agg,
+                        float* post, uint32_t* hb, void* stream);
+/* kernels qc_decode launches for these arguments (bench accounting) */
+QC_API int qc_decode_launches(const qc_plan* plan, int gamma, int iters, int early_stop);
 
 /* lane-major outputs (DecodeResult / DecodedFrame layout, bp.py:87-100,
  * convolutional.py:166-177): post (n, gamma) fp32 -> post_out (gamma_out, n)

@@ -13,7 +13,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libqcldpc_b200.so")
+LIB_PATH = os.environ.get("QCB_LIB_PATH") or os.path.join(HERE, "lib", "libqcldpc_b200.so")  # override: A/B builds
 
 _p = C.c_void_p
 _i = C.c_int
@@ -37,8 +37,12 @@ SIGNATURES = {
     "qc_syndrome": (_i, [_p, _i, _p, _p, _p]),
     "qc_hard_bits": (_i, [_p, _i, _p, _p, _p]),
     "qc_bit_errors": (_i, [_p, _i, _p, _p, _p]),
-    "qc_decode_work_words": (C.c_size_t, [_i]),
+    "qc_decode_work_words": (C.c_size_t, [_p, _i]),
     "qc_decode": (_i, [_p, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "qc_agg_check": (_i, [_p, _i, _i, _p, _p, _p, _p]),
+    "qc_agg_var": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p]),
+    "qc_agg_fused": (_i, [_p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p]),
+    "qc_decode_launches": (_i, [_p, _i, _i, _i]),
     "qc_lane_major": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_lane_major_f32": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_llr_from_lane_major": (_i, [_i, _i, _i, _p, _d, _p, _p]),

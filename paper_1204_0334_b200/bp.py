@@ -189,7 +189,7 @@ class BlockDecoder:
         self.msgs = torch.zeros((E, gp), dtype=f32, device=dev)
         self.post = torch.zeros((N, gp), dtype=f32, device=dev)
         self.hb = torch.zeros((N, gp // 32), dtype=i32, device=dev)
-        self.work = torch.zeros(int(_lib.load().qc_decode_work_words(gp)), dtype=i32, device=dev)
+        self.work = torch.zeros(int(_lib.load().qc_decode_work_words(self.plan.handle, gp)), dtype=i32, device=dev)
         self.ok = torch.zeros(gp, dtype=torch.uint8, device=dev)
         self.iters = torch.zeros(gp, dtype=i32, device=dev)
         self.lane_bits = torch.zeros(gp, dtype=i32, device=dev) if count_bits else None
@@ -231,11 +231,12 @@ class BlockDecoder:
 
     def kernel_launches_per_run(self) -> int:
         """Our kernels in one run() (for bench gpu_launches)."""
-        it = self.iterations
-        if self.early_stop:
-            n = 2 + 4 * it + 2       # start, init, it x (cnu, vnu, syndrome, freeze), ok, bits
+        if self.fp64:
+            it = self.iterations
+            n = (2 + 4 * it + 2) if self.early_stop else (1 + 2 * it + 2)
         else:
-            n = 1 + 2 * it + 2       # fill, it x (cnu, vnu), syndrome, ok
+            n = int(_lib.load().qc_decode_launches(self.plan.handle, self.gp, self.iterations,
+                                                   int(self.early_stop)))
         if self.lane_bits is not None:
             n += 1
         return n

@@ -23,7 +23,7 @@ OUT_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(OUT_DIR, "libqcldpc_b200.so")
 SOURCES = ["plan.cu", "block.cu", "vnu.cu", "cnu_dc4.cu", "cnu_dc8.cu", "cnu_dc16.cu", "cnu_dc24.cu",
            "cnu_dc32.cu", "cnu_pipe.cu", "recycle.cu", "block64.cu", "channel.cu", "stream.cu",
-           "host_pipe.cu"]
+           "host_pipe.cu", "agg.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden"]
@@ -43,9 +43,12 @@ def _stale(obj: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB) -> str:
+    """Compile into `lib`; `defines` (e.g. ["-DAGG_VAR_MINB=1"]) build an A/B
+    variant into its own object directory."""
     nvcc = _nvcc()
-    obj_dir = os.path.join(OUT_DIR, "obj")
+    tag = "".join(d.strip("-D").replace("=", "") for d in defines)
+    obj_dir = os.path.join(OUT_DIR, "obj" + (("_" + tag) if tag else ""))
     os.makedirs(obj_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "qcldpc_b200.h"))
@@ -54,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(obj_dir, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + headers):
-            jobs.append([nvcc, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([nvcc, *ARCH, *FLAGS, *defines, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,11 +69,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
         list(ex.map(run, jobs))
     objs = [os.path.join(obj_dir, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _stale(LIB, objs):
-        tmp = LIB + ".tmp"
+    if force or jobs or _stale(lib, objs):
+        os.makedirs(os.path.dirname(lib), exist_ok=True)
+        tmp = lib + ".tmp"
         run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -1,0 +1,546 @@
+// Compact-check-state flooding schedule for regular QC codes (the production
+// decode loop inside qc_decode, fixed iteration count).
+//
+// The reference alternates check_node_update / variable_node_update over one
+// (E, gamma) package store (bp.py:134-188): the check pass reads and rewrites
+// every package, the variable pass gathers them again -- 4E + N package
+// transfers per iteration.  A check's outgoing messages are a function of four
+// per-(check, lane) numbers and of each edge's own incoming message:
+//     S   = sum_k psi_k            (psi = phi(|beta|)/ln2, the phi form)
+//     S2  = S without its first maximum (accumulated directly: no cancellation)
+//     mx  = max_k psi_k
+//     par = XOR of the signs
+//     alpha_k = sign(par ^ sign_k) * min(phi((psi_k == mx) ? S2 : S - psi_k), cap)
+// so the check pass here writes only (S|par, S2, mx) per check and lane
+// (3 words instead of d_c packages), and the variable pass re-derives alpha_k
+// from them and the package it is about to overwrite.  The arithmetic is the
+// same instruction sequence as cnu_core + vnu_kernel (block_kernels.cuh), so
+// results are bit-identical to the two-pass schedule; the package store
+// traffic drops from 4E + N to 3E + N (+ 6M) words per lane and iteration.
+//
+// Thread mapping (both passes): lane-group major -- all rows (checks or
+// variables) of lanes [g*LG, (g+1)*LG) before the next lane group, so the
+// check records a variable pass gathers (24 reads per record) stay L2
+// resident: LG = 512 lanes -> 3060 x 512 x 12 B = 18.8 MB for n18360.
+#include <cstdlib>
+
+#include "block_kernels.cuh"
+
+namespace qcb {
+
+struct AggArgs {
+  float* msgs;         // (E, gamma) phi-form var->check packages
+  const float* mu;     // (N, gamma) channel LLRs
+  float* agg;          // (M, 3, gamma): S|par, S2, mx
+  float* post;         // (N, gamma) or null
+  uint32_t* hb;        // (N, gamma/32) or null
+  int rows, gamma;     // rows = M (check pass) or N (variable pass); gamma = row stride in lanes
+  int q0;              // first lane vector of this pass's lane window
+  int lg_gw;           // log2(lane vectors per group)
+  int groups;          // lane groups in the window
+  int reverse;         // visit lane groups last-to-first
+};
+
+// min CTAs/SM for the variable job: 4 x 256 threads caps it at 64 registers,
+// enough to issue all 17 loads of an item before its arithmetic (measured best
+// on B200: 2 -> 88 regs / 16 warps is 15% slower, 5 -> 48 regs spills)
+#ifndef AGG_VAR_MINB
+#define AGG_VAR_MINB 4
+#endif
+
+enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
+
+// block (bx within its lane group, group index) + thread -> (row, lane vector q).
+// Lane-group major: every row of one group of lanes before the next group.
+__device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned grp, int& row, int& q) {
+  const unsigned idx = bx * THREADS + threadIdx.x;
+  row = (int)(idx >> a.lg_gw);
+  if (row >= a.rows) return false;
+  const int g = a.reverse ? a.groups - 1 - (int)grp : (int)grp;
+  q = a.q0 + (g << a.lg_gw) + (int)(idx & ((1u << a.lg_gw) - 1u));
+  return true;
+}
+
+template <int DC, int VEC, bool FROM_MU>
+__device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid, int m, int q) {
+  int jrow = 0, r = 0;
+  if constexpr (FROM_MU) {
+    jrow = div_p(grid, m);
+    r = m - jrow * grid.p;
+  }
+  float x[DC][VEC];
+#pragma unroll
+  for (int k = 0; k < DC; ++k) {
+    if constexpr (FROM_MU) {
+      int c = r + grid.s[jrow * grid.L + k];
+      c -= (c >= grid.p) ? grid.p : 0;
+      vload<VEC>(a.mu + (size_t)(k * grid.p + c) * a.gamma + q * VEC, x[k]);
+    } else {
+      vload<VEC>(a.msgs + (size_t)(m * DC + k) * a.gamma + q * VEC, x[k]);
+    }
+  }
+  float oS[VEC], oS2[VEC], oM[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    unsigned par = 0;
+    float S = 0.0f, S2 = 0.0f, mx = -1.0f;
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+      float b = x[k][i];
+      unsigned sb = __float_as_uint(b) & 0x80000000u;
+      float f = FROM_MU ? psi_of_nat(fabsf(b)) : fabsf(b);
+      par ^= sb;
+      S2 = (f > mx) ? S : __fadd_rn(S2, f);
+      mx = fmaxf(mx, f);
+      S = __fadd_rn(S, f);
+    }
+    oS[i] = __uint_as_float(__float_as_uint(S) | par);
+    oS2[i] = S2;
+    oM[i] = mx;
+  }
+  float* rec = a.agg + (size_t)m * 3 * a.gamma + q * VEC;
+  vstore<VEC>(rec, oS);
+  vstore<VEC>(rec + a.gamma, oS2);
+  vstore<VEC>(rec + 2 * a.gamma, oM);
+}
+
+template <int DV, int VEC, int FLAGS>
+__device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, int n, int q) {
+  const int l = div_p(grid, n), c = n - l * grid.p;
+  int mrow[DV];
+#pragma unroll
+  for (int j = 0; j < DV; ++j) {
+    int rr = c - grid.s[j * grid.L + l];
+    rr += (rr < 0) ? grid.p : 0;
+    mrow[j] = j * grid.p + rr;
+  }
+  float tot[VEC], v2c[DV][VEC], al[DV][VEC];
+  vload<VEC>(a.mu + (size_t)n * a.gamma + q * VEC, tot);
+  if constexpr (FLAGS & AGG_FIRST) {
+    // beta^0 = mu on every edge, in the phi form the fused-init check pass saw
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      float p0 = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(tot[i]))) |
+                                 (__float_as_uint(tot[i]) & 0x80000000u));
+#pragma unroll
+      for (int j = 0; j < DV; ++j) v2c[j][i] = p0;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < DV; ++j)
+      vload<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, v2c[j]);
+  }
+  // every load of the item is issued before any arithmetic (one memory round
+  // trip per item; the compiler otherwise interleaves them with the phi math)
+  float sS[DV][VEC], sS2[DV][VEC], sM[DV][VEC];
+#pragma unroll
+  for (int j = 0; j < DV; ++j) {
+    const float* rec = a.agg + (size_t)mrow[j] * 3 * a.gamma + q * VEC;
+    vload<VEC>(rec, sS[j]);
+    vload<VEC>(rec + a.gamma, sS2[j]);
+    vload<VEC>(rec + 2 * a.gamma, sM[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < DV; ++j) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      unsigned u = __float_as_uint(v2c[j][i]);
+      unsigned sp = __float_as_uint(sS[j][i]);
+      float f = __uint_as_float(u & 0x7fffffffu);
+      float S = __uint_as_float(sp & 0x7fffffffu);
+      float mag = (f == sM[j][i]) ? sS2[j][i] : __fsub_rn(S, f);
+      float al_ = fminf(phi_of_log2(mag), ALPHA_CAP);
+      al[j][i] = __uint_as_float(__float_as_uint(al_) | ((u ^ sp) & 0x80000000u));
+    }
+  }
+  // running total in increasing edge order (bp.py:179-181)
+#pragma unroll
+  for (int j = 0; j < DV; ++j)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
+  if constexpr (!(FLAGS & AGG_LAST)) {
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      float b[VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        float beta = clampL(__fsub_rn(tot[i], al[j][i]));
+        b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+      }
+      vstore<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, b);
+    }
+  } else {
+    float pst[VEC];
+    unsigned bits = 0;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      pst[i] = clampL(tot[i]);
+      bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
+    }
+    if (a.post) vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
+    // whole warps share one row (gw >= 32), so the shuffle is safe
+    if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, true);
+  }
+}
+
+// grid = (blocks per lane group, groups)
+template <int DC, int VEC, bool FROM_MU>
+__global__ void __launch_bounds__(THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+  int m, q;
+  if (agg_map(a, blockIdx.x, blockIdx.y, m, q)) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
+}
+
+template <int DV, int VEC, int FLAGS>
+__global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+  int n, q;
+  if (agg_map(a, blockIdx.x, blockIdx.y, n, q)) var_body<DV, VEC, FLAGS>(a, grid, n, q);
+}
+
+// One launch, two independent jobs on disjoint lane windows: the variable pass
+// of window v (compute-heavy: 2 phi per edge-lane) and the check pass of window
+// c (pure streaming).  Grid (R + 1, nbc): x = 0..R-1 are variable blocks
+// y*R + x, x = R is check block y, so the block scheduler interleaves the two
+// kinds and every SM mixes MUFU-bound and HBM-bound CTAs.
+struct FusedArgs {
+  AggArgs v, c;
+  unsigned R, nbv;                          // variable blocks per row of the grid, total
+  unsigned v_bpg, c_bpg;                    // blocks per lane group
+  unsigned long long v_magic, c_magic;      // ceil(2^40 / bpg)
+};
+
+__device__ __forceinline__ unsigned div_magic(unsigned x, unsigned long long m) {
+  return (unsigned)(((unsigned long long)x * m) >> 40);
+}
+
+template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS>
+__global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
+  int row, q;
+  if (blockIdx.x == f.R) {
+    const unsigned b = blockIdx.y, g = div_magic(b, f.c_magic);
+    if (agg_map(f.c, b - g * f.c_bpg, g, row, q)) check_body<DC, VC, FROM_MU>(f.c, grid, row, q);
+  } else {
+    const unsigned b = blockIdx.y * f.R + blockIdx.x;
+    if (b >= f.nbv) return;
+    const unsigned g = div_magic(b, f.v_magic);
+    if (agg_map(f.v, b - g * f.v_bpg, g, row, q)) var_body<DV, VV, FLAGS>(f.v, grid, row, q);
+  }
+}
+
+namespace {
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+int agg_mode() {
+  static int v = env_int("QCB_AGG", 1);   // 0 = two-pass schedule (A/B experiments)
+  return v;
+}
+int agg_lanes() {
+  static int v = env_int("QCB_AGG_LG", 128);
+  return v;
+}
+int agg_tile() {
+  static int v = env_int("QCB_AGG_TILE", 0);   // >0: lanes decoded together (measured: no gain, the strided tile rows cost more)
+  return v;
+}
+int agg_reverse() {
+  static int v = env_int("QCB_AGG_REV", 1);
+  return v;
+}
+int agg_fused_mode() {
+  static int v = env_int("QCB_AGG_FUSED", 1);    // 0 = unfused compact passes
+  return v;
+}
+int agg_vv() {
+  static int v = env_int("QCB_AGG_VV", 4);       // lanes per thread of the variable job (4 or 2)
+  return v == 2 ? 2 : 4;
+}
+int agg_fused_vc() {
+  static int v = env_int("QCB_AGG_FVC", 2);      // lanes per thread of the fused check job
+  return v == 4 ? 4 : 2;
+}
+
+bool dc_supported(int dc) { return dc == 4 || dc == 6 || dc == 8 || dc == 12 || dc == 16 || dc == 24 || dc == 32; }
+bool dv_supported(int dv) { return dv >= 2 && dv <= 4; }
+
+int pick_vec(int gamma) { return gamma % 128 == 0 ? 4 : (gamma % 64 == 0 ? 2 : 1); }
+int pick_vec_var(int gamma) { return std::min(pick_vec(gamma), agg_vv()); }
+
+// log2 of the lane vectors per group: the largest power of two <= LG/VEC that
+// divides GV = gamma/VEC (GV is a multiple of 32 for every vec pick_vec returns)
+int pick_lg_gw(int gamma, int vec) {
+  int GV = gamma / vec, target = std::max(32, agg_lanes() / vec), lg = 5;
+  while ((2 << lg) <= target && GV % (2 << lg) == 0) ++lg;
+  return lg;
+}
+
+unsigned blocks_per_group(const AggArgs& a) {
+  return (unsigned)((((long long)a.rows << a.lg_gw) + THREADS - 1) / THREADS);
+}
+
+dim3 agg_grid(const AggArgs& a, int) { return dim3(blocks_per_group(a), (unsigned)a.groups, 1); }
+
+// pass arguments over the lane window [lane0, lane0 + lanes) of a gamma-wide store
+AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_t* hb, int rows, int gamma,
+                  int lane0, int lanes, int vec, int reverse) {
+  AggArgs a{msgs, mu, agg, post, hb, rows, gamma, lane0 / vec, pick_lg_gw(lanes, vec), 0, reverse};
+  a.groups = (lanes / vec) >> a.lg_gw;
+  return a;
+}
+
+template <int DC, int VEC>
+void launch_check_v(const AggArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
+  dim3 nb = agg_grid(a, VEC);
+  if (from_mu) agg_check_kernel<DC, VEC, true><<<nb, THREADS, 0, s>>>(a, g);
+  else agg_check_kernel<DC, VEC, false><<<nb, THREADS, 0, s>>>(a, g);
+}
+
+template <int DC>
+void launch_check_dc(const AggArgs& a, int vec, bool from_mu, const QcGrid& g, cudaStream_t s) {
+  switch (vec) {
+    case 4: launch_check_v<DC, 4>(a, from_mu, g, s); break;
+    case 2: launch_check_v<DC, 2>(a, from_mu, g, s); break;
+    default: launch_check_v<DC, 1>(a, from_mu, g, s);
+  }
+}
+
+template <int DV, int VEC>
+void launch_var_v(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
+  dim3 nb = agg_grid(a, VEC);
+  switch (flags) {
+    case 0: agg_var_kernel<DV, VEC, 0><<<nb, THREADS, 0, s>>>(a, g); break;
+    case AGG_FIRST: agg_var_kernel<DV, VEC, AGG_FIRST><<<nb, THREADS, 0, s>>>(a, g); break;
+    case AGG_LAST: agg_var_kernel<DV, VEC, AGG_LAST><<<nb, THREADS, 0, s>>>(a, g); break;
+    default: agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST><<<nb, THREADS, 0, s>>>(a, g);
+  }
+}
+
+template <int DV>
+void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaStream_t s) {
+  switch (vec) {
+    case 4: launch_var_v<DV, 4>(a, flags, g, s); break;
+    case 2: launch_var_v<DV, 2>(a, flags, g, s); break;
+    default: launch_var_v<DV, 1>(a, flags, g, s);
+  }
+}
+
+template <int DC, int DV, int VC, bool FROM_MU, int FLAGS>
+void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t s) {
+  if (agg_vv() == 2) agg_fused_kernel<DC, DV, VC, 2, FROM_MU, FLAGS><<<grid, THREADS, 0, s>>>(f, g);
+  else agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS><<<grid, THREADS, 0, s>>>(f, g);
+}
+
+template <int DC, int DV, int VC>
+int launch_fused_v(const FusedArgs& f, dim3 grid, bool from_mu, int flags, const QcGrid& g, cudaStream_t s) {
+  if (from_mu && flags == AGG_FIRST) launch_fused_t<DC, DV, VC, true, AGG_FIRST>(f, grid, g, s);
+  else if (from_mu && flags == (AGG_FIRST | AGG_LAST)) launch_fused_t<DC, DV, VC, true, AGG_FIRST | AGG_LAST>(f, grid, g, s);
+  else if (!from_mu && flags == AGG_FIRST) launch_fused_t<DC, DV, VC, false, AGG_FIRST>(f, grid, g, s);
+  else if (!from_mu && flags == 0) launch_fused_t<DC, DV, VC, false, 0>(f, grid, g, s);
+  else if (!from_mu && flags == AGG_LAST) launch_fused_t<DC, DV, VC, false, AGG_LAST>(f, grid, g, s);
+  else return fail_arg("fused compact pass: unsupported (from_mu, flags) combination");
+  return 0;
+}
+
+template <int DC, int DV>
+int launch_fused_dc(const FusedArgs& f, dim3 grid, int vc, bool from_mu, int flags, const QcGrid& g,
+                    cudaStream_t s) {
+  return vc == 4 ? launch_fused_v<DC, DV, 4>(f, grid, from_mu, flags, g, s)
+                 : launch_fused_v<DC, DV, 2>(f, grid, from_mu, flags, g, s);
+}
+
+unsigned long long magic40(unsigned d) { return ((1ull << 40) + d - 1) / d; }
+
+}  // namespace
+
+bool agg_fused_eligible(const qc_plan* p, int gamma) {
+  return agg_fused_mode() != 0 && agg_eligible(p) && gamma % 256 == 0 &&
+         ((p->L == 24 && p->J == 4) || (p->L == 4 && p->J == 2));
+}
+
+// variable pass on lanes [v0, v0 + lanes) fused with the check pass on lanes [c0, c0 + lanes)
+int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
+                     const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s) {
+  const int vc = agg_fused_vc();
+  FusedArgs f;
+  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, agg_vv(), agg_reverse());
+  f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, vc, 0);
+  f.v_bpg = blocks_per_group(f.v);
+  f.c_bpg = blocks_per_group(f.c);
+  f.v_magic = magic40(f.v_bpg);
+  f.c_magic = magic40(f.c_bpg);
+  f.nbv = f.v_bpg * f.v.groups;
+  const unsigned nbc = f.c_bpg * f.c.groups;
+  f.R = (f.nbv + nbc - 1) / nbc;
+  const dim3 grid(f.R + 1, nbc, 1);
+  const QcGrid g = make_grid(p);
+  int rc = (p->L == 24) ? launch_fused_dc<24, 4>(f, grid, vc, from_mu, flags, g, s)
+                        : launch_fused_dc<4, 2>(f, grid, vc, from_mu, flags, g, s);
+  if (rc) return rc;
+  return check_launch("agg_fused");
+}
+
+// single passes over a lane window
+int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
+                       const float* mu, float* agg, cudaStream_t s);
+int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
+                     const float* agg, float* post, uint32_t* hb, cudaStream_t s);
+
+bool agg_eligible(const qc_plan* p) {
+  return agg_mode() != 0 && p && p->qc_regular && p->E > 0 && dc_supported(p->L) && dv_supported(p->J) &&
+         p->check_regular == p->L;
+}
+
+size_t agg_words(const qc_plan* p, int gamma) {
+  return agg_eligible(p) ? (size_t)3 * p->M * (size_t)(gamma > 0 ? gamma : 0) : 0;
+}
+
+int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, const float* mu, float* agg,
+                     cudaStream_t s) {
+  return launch_agg_check_w(p, gamma, 0, gamma, from_mu, msgs, mu, agg, s);
+}
+
+int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
+                       const float* mu, float* agg, cudaStream_t s) {
+  const int vec = pick_vec(lanes);
+  AggArgs a = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, lane0, lanes, vec, 0);
+  const QcGrid g = make_grid(p);
+  switch (p->L) {
+    case 4: launch_check_dc<4>(a, vec, from_mu, g, s); break;
+    case 6: launch_check_dc<6>(a, vec, from_mu, g, s); break;
+    case 8: launch_check_dc<8>(a, vec, from_mu, g, s); break;
+    case 12: launch_check_dc<12>(a, vec, from_mu, g, s); break;
+    case 16: launch_check_dc<16>(a, vec, from_mu, g, s); break;
+    case 24: launch_check_dc<24>(a, vec, from_mu, g, s); break;
+    case 32: launch_check_dc<32>(a, vec, from_mu, g, s); break;
+    default: return fail_arg("compact schedule: unsupported check degree");
+  }
+  return check_launch("agg_check");
+}
+
+int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const float* mu, const float* agg,
+                   float* post, uint32_t* hb, cudaStream_t s) {
+  return launch_agg_var_w(p, gamma, 0, gamma, flags, msgs, mu, agg, post, hb, s);
+}
+
+int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
+                     const float* agg, float* post, uint32_t* hb, cudaStream_t s) {
+  const int vec = pick_vec_var(lanes);
+  AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
+                        agg_reverse());
+  const QcGrid g = make_grid(p);
+  switch (p->J) {
+    case 2: launch_var_dv<2>(a, vec, flags, g, s); break;
+    case 3: launch_var_dv<3>(a, vec, flags, g, s); break;
+    case 4: launch_var_dv<4>(a, vec, flags, g, s); break;
+    default: return fail_arg("compact schedule: unsupported variable degree");
+  }
+  return check_launch("agg_var");
+}
+
+// The whole fixed-iteration flooding loop on the compact schedule.  With the
+// fused kernel the lanes split into halves A and B that run half an iteration
+// apart: launch k is var(X, t) + check(Y, t') so every launch mixes the
+// compute-heavy variable job of one half with the streaming check job of the
+// other (2 iters + 1 launches).  Bit-identical to the unfused passes.
+int run_agg_tile(const qc_plan* p, int gamma, int lane0, int lanes, int iters, float* msgs, const float* mu,
+                 float* agg, float* post, uint32_t* hb, cudaStream_t s);
+
+// Lanes are decoded in tiles of agg_tile() lanes, one complete flooding loop
+// per tile: a tile's check records (3 M x tile words, 37 MB for n18360 at 1024
+// lanes) stay L2-resident between the passes.
+int run_agg_decode(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
+                   uint32_t* hb, cudaStream_t s) {
+  const int T = agg_tile_lanes(p, gamma);
+  for (int l0 = 0; l0 < gamma; l0 += T)
+    if (int rc = run_agg_tile(p, gamma, l0, std::min(T, gamma - l0), iters, msgs, mu, agg, post, hb, s)) return rc;
+  return 0;
+}
+
+int agg_tile_lanes(const qc_plan* p, int gamma) {
+  const int t = agg_tile();
+  if (t <= 0 || t >= gamma || t % 256 || gamma % t || !agg_fused_eligible(p, gamma)) return gamma;
+  return t;
+}
+
+int run_agg_tile(const qc_plan* p, int gamma, int lane0, int lanes, int iters, float* msgs, const float* mu,
+                 float* agg, float* post, uint32_t* hb, cudaStream_t s) {
+  int rc;
+  if (!agg_fused_eligible(p, lanes)) {
+    for (int it = 1; it <= iters; ++it) {
+      if ((rc = launch_agg_check_w(p, gamma, lane0, lanes, it == 1, msgs, mu, agg, s))) return rc;
+      int flags = (it == 1 ? AGG_FIRST : 0) | (it == iters ? AGG_LAST : 0);
+      if ((rc = launch_agg_var_w(p, gamma, lane0, lanes, flags, msgs, mu, agg, it == iters ? post : nullptr,
+                                 it == iters ? hb : nullptr, s)))
+        return rc;
+    }
+    return 0;
+  }
+  const int H = lanes / 2, A = lane0, B = lane0 + H;
+  if ((rc = launch_agg_check_w(p, gamma, A, H, true, msgs, mu, agg, s))) return rc;
+  for (int t = 1; t <= iters; ++t) {
+    const int vflags = (t == 1 ? AGG_FIRST : 0) | (t == iters ? AGG_LAST : 0);
+    float* po = t == iters ? post : nullptr;
+    uint32_t* ho = t == iters ? hb : nullptr;
+    // var(A, t) + check(B, t)
+    if ((rc = launch_agg_fused(p, gamma, H, A, vflags, B, t == 1, msgs, mu, agg, po, ho, s))) return rc;
+    if (t < iters) {
+      // var(B, t) + check(A, t + 1)
+      if ((rc = launch_agg_fused(p, gamma, H, B, vflags, A, false, msgs, mu, agg, po, ho, s))) return rc;
+    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, po, ho, s))) {
+      return rc;
+    }
+  }
+  return 0;
+}
+
+int agg_decode_launches(const qc_plan* p, int gamma, int iters) {
+  const int T = agg_tile_lanes(p, gamma);
+  return (gamma / T) * (agg_fused_eligible(p, T) ? 2 * iters + 1 : 2 * iters);
+}
+
+}  // namespace qcb
+
+// ============================================================================
+// C ABI: the two passes of the compact schedule on their own (tests, benches)
+// ============================================================================
+extern "C" {
+
+int qc_agg_check(const qc_plan* p, int gamma, int from_mu, float* msgs, const float* mu, float* agg,
+                 void* stream) {
+  if (!p || !agg || (from_mu ? !mu : !msgs)) return qcb::fail_arg("null argument");
+  if (gamma <= 0 || gamma % 32) return qcb::fail_arg("gamma must be a positive multiple of 32");
+  if (!qcb::agg_eligible(p)) return qcb::fail_arg("compact schedule needs a regular QC plan");
+  return qcb::launch_agg_check(p, gamma, from_mu != 0, msgs, mu, agg, qcb::as_stream(stream));
+}
+
+int qc_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const float* mu, const float* agg,
+               float* post, uint32_t* hb, void* stream) {
+  if (!p || !agg || !mu || !msgs) return qcb::fail_arg("null argument");
+  if (gamma <= 0 || gamma % 32) return qcb::fail_arg("gamma must be a positive multiple of 32");
+  if (flags < 0 || flags > 3) return qcb::fail_arg("flags: 1 = first iteration, 2 = last iteration");
+  if (!qcb::agg_eligible(p)) return qcb::fail_arg("compact schedule needs a regular QC plan");
+  return qcb::launch_agg_var(p, gamma, flags, msgs, mu, agg, post, hb, qcb::as_stream(stream));
+}
+
+int qc_agg_fused(const qc_plan* p, int gamma, int lanes, int var_lane0, int var_flags, int check_lane0,
+                 int check_from_mu, float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
+                 void* stream) {
+  if (!p || !agg || !mu || !msgs) return qcb::fail_arg("null argument");
+  if (gamma <= 0 || gamma % 256) return qcb::fail_arg("fused compact pass: gamma must be a multiple of 256");
+  if (lanes <= 0 || lanes % 128 || var_lane0 % 128 || check_lane0 % 128 || var_lane0 < 0 || check_lane0 < 0 ||
+      var_lane0 + lanes > gamma || check_lane0 + lanes > gamma)
+    return qcb::fail_arg("fused compact pass: lane windows must be 128-lane aligned and inside gamma");
+  if (!qcb::agg_fused_eligible(p, gamma)) return qcb::fail_arg("fused compact pass: unsupported plan");
+  return qcb::launch_agg_fused(p, gamma, lanes, var_lane0, var_flags, check_lane0, check_from_mu != 0, msgs, mu,
+                               agg, post, hb, qcb::as_stream(stream));
+}
+
+int qc_decode_launches(const qc_plan* p, int gamma, int iters, int early_stop) {
+  if (!p || iters < 1) return -1;
+  if (!early_stop && qcb::agg_eligible(p)) return 3 + qcb::agg_decode_launches(p, gamma, iters);
+  return early_stop ? 2 + 4 * iters + 2 : 1 + 2 * iters + 2;
+}
+
+}  // extern "C"

@@ -330,10 +330,11 @@ int qc_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane
   return launch_bit_errors(p, gamma, hb, lane_bits, as_stream(stream));
 }
 
-size_t qc_decode_work_words(int gamma) {
-  // bad (W) | active (W) | done (1) | pad
+size_t qc_decode_work_words(const qc_plan* p, int gamma) {
+  // bad (W) | active (W) | done (1) | pad to 64 words | check records (agg.cu)
   size_t W = (size_t)(gamma > 0 ? gamma : 0) / 32;
-  return 2 * W + 4;
+  size_t head = (2 * W + 4 + 63) / 64 * 64;
+  return head + agg_words(p, gamma);
 }
 
 int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const float* mu, float* msgs,
@@ -350,7 +351,15 @@ int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const floa
   int rc = 0;
   // Messages between the passes are kept in PHI form (sign * phi(|beta|)):
   // iteration 1 reads beta^0 = mu straight from the LLRs (fused init).
-  if (!early_stop) {
+  if (!early_stop && agg_eligible(p)) {
+    // compact check-state schedule (agg.cu): bit-identical, fewer package bytes
+    float* agg = reinterpret_cast<float*>(work + (2 * (size_t)W + 4 + 63) / 64 * 64);
+    cudaMemsetAsync(bad, 0, sizeof(uint32_t) * W, s);
+    fill_i32<<<blocks_for(gamma), THREADS, 0, s>>>(iters_run, gamma, iters);
+    if ((rc = run_agg_decode(p, gamma, iters, msgs, mu, agg, post, hb, s))) return rc;
+    if ((rc = launch_syndrome(p, gamma, hb, bad, nullptr, s))) return rc;
+    finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, nullptr, ok, gamma);
+  } else if (!early_stop) {
     cudaMemsetAsync(bad, 0, sizeof(uint32_t) * W, s);
     fill_i32<<<blocks_for(gamma), THREADS, 0, s>>>(iters_run, gamma, iters);
     for (int it = 1; it <= iters; ++it) {

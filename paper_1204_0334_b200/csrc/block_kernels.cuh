@@ -30,8 +30,13 @@ namespace qcb {
 // (no shared-memory staging, no CTA barrier).
 struct QcGrid {
   int J, L, p;
+  unsigned long long pmagic;   // ceil(2^40 / p): x / p == (x * pmagic) >> 40 for x < 2^24
   int16_t s[QC_MAX_J * QC_MAX_L];
 };
+
+__device__ __forceinline__ int div_p(const QcGrid& g, int x) {
+  return (int)(((unsigned long long)(unsigned)x * g.pmagic) >> 40);
+}
 
 enum CnuMode { CNU_BETA = 0, CNU_FROM_MU = 1, CNU_PHI = 2 };
 enum VnuMode { VNU_BETA = 0, VNU_PHI = 1, VNU_NONE = 2 };
@@ -238,6 +243,22 @@ QcGrid make_grid(const qc_plan* p);
 // persistent cp.async-pipelined check pass (cnu_pipe.cu); 0 if not applicable
 int launch_cnu_phi_pipe(const qc_plan* p, const CnuArgs& a, cudaStream_t s);
 int cnu_pipe_mode();   // QCB_CNU_PIPE env: 1 = use the pipelined check pass
+
+// compact check-state schedule (agg.cu)
+constexpr int AGG_FIRST_FLAG = 1, AGG_LAST_FLAG = 2;
+bool agg_eligible(const qc_plan* p);
+size_t agg_words(const qc_plan* p, int gamma);
+int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, const float* mu, float* agg,
+                     cudaStream_t s);
+int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const float* mu, const float* agg,
+                   float* post, uint32_t* hb, cudaStream_t s);
+int run_agg_decode(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
+                   uint32_t* hb, cudaStream_t s);
+int agg_decode_launches(const qc_plan* p, int gamma, int iters);
+int agg_tile_lanes(const qc_plan* p, int gamma);
+bool agg_fused_eligible(const qc_plan* p, int gamma);
+int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
+                     const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s);
 
 template <int DC>
 int launch_cnu_dc(const qc_plan* p, const CnuArgs& a, int mode, cudaStream_t s);

@@ -137,7 +137,7 @@ static int init_slot(qc_host_dec* h, Slot& s) {
   HP_CK(cudaMalloc(&s.msgs, E * C * sizeof(float)));
   HP_CK(cudaMalloc(&s.post, N * C * sizeof(float)));
   HP_CK(cudaMalloc(&s.hb, N * (C / 32) * sizeof(uint32_t)));
-  HP_CK(cudaMalloc(&s.work, qc_decode_work_words(h->chunk) * sizeof(uint32_t)));
+  HP_CK(cudaMalloc(&s.work, qc_decode_work_words(p, h->chunk) * sizeof(uint32_t)));
   HP_CK(cudaMalloc(&s.ok, C));
   HP_CK(cudaMalloc(&s.its, C * sizeof(int32_t)));
   HP_CK(cudaMalloc(&s.post_lm, C * N * sizeof(double)));

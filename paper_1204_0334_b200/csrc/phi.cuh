@@ -76,17 +76,18 @@ __device__ __forceinline__ float psi_of_nat(float x) {
   return (t < 0.03125f) ? ps : pl;
 }
 
-// phi(y ln2), natural-log-domain result, for a log2-domain argument y >= 0
+// phi(y ln2), natural-log-domain result, for a log2-domain argument y >= 0.
+// This is the check-to-variable magnitude |alpha|: it only ever enters sums
+// (totals, extrinsics), so it needs ABSOLUTE accuracy, not relative accuracy
+// for tiny results -- the lg2 form is within ~3e-7 absolute everywhere and the
+// small-t series of psi_of_nat is not needed here (6 instructions per edge).
 __device__ __forceinline__ float phi_of_log2(float y) {
   const float LN2 = 0.6931471805599453f;
   float t = ex2a(-y);
   float ms = __fmul_rn(y, fmaf(y, fmaf(y, 0.055504108664821580f /* ln2^3/6 */, -0.24022650695910071f /* -ln2^2/2 */),
                                LN2));
   float m = (y < 0.011270696f /* 2^-7 / ln2 */) ? fmaxf(ms, 1e-30f) : __fsub_rn(1.0f, t);
-  float pl = __fmul_rn(lg2a(__fmul_rn(__fsub_rn(2.0f, m), rcpa(m))), LN2);
-  float t2 = __fmul_rn(t, t);
-  float ps = __fmul_rn(t, fmaf(t2, fmaf(t2, 0.4f, 2.0f / 3.0f), 2.0f));
-  return (t < 0.03125f) ? ps : pl;
+  return __fmul_rn(lg2a(__fmul_rn(__fsub_rn(2.0f, m), rcpa(m))), LN2);
 }
 
 }  // namespace qcb

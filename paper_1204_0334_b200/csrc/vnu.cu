@@ -20,6 +20,7 @@ QcGrid make_grid(const qc_plan* p) {
   std::memset(&g, 0, sizeof(g));
   if (p->qc_regular) {
     g.J = p->J; g.L = p->L; g.p = p->p;
+    g.pmagic = ((1ull << 40) + (unsigned long long)p->p - 1) / (unsigned long long)p->p;
     for (int i = 0; i < p->J * p->L; ++i) g.s[i] = (int16_t)p->shifts[i];
   }
   return g;

@@ -42,7 +42,7 @@ def test_argument_errors_map_to_value_error():
         _lib.check(rc)
     rc = lib.cc_plan_create(sh.ctypes.data_as(C.c_void_p), 1, 3, 11, C.byref(h))
     assert rc < 0 and b"gcd" in lib.qc_last_error()
-    assert lib.qc_decode_work_words(64) == 8
+    assert lib.qc_decode_work_words(None, 64) == 64          # no plan: header words only
     assert lib.qc_cnu(None, 33, None, None, None) < 0          # gamma not a multiple of 32
 
 

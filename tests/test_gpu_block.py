@@ -274,3 +274,76 @@ def test_pipelined_check_pass_is_bit_identical(gpu, tmp_path):
         subprocess.run([sys.executable, "-c", _PIPE_SNIPPET, f], cwd=REPO, env=env, check=True)
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_compact_schedule_passes_are_bit_identical(gpu):
+    """qc_agg_check + qc_agg_var (compact check records) == qc_cnu_ex(phi) +
+    qc_vnu_ex(phi) on the same phi-form packages, bit for bit; also the fused
+    first iteration (records from mu) and the last (posteriors + hard bits)."""
+    import torch
+    q = gpu
+    from paper_1204_0334_b200 import _lib
+    for name, G in (("n18360", 256), ("code_c_like", 96)):
+        h, exp = q.load_code(q.codes.bundled_code_path(name))
+        lay = q.build_edge_layout(h)
+        N, M, E = lay.n_vars, lay.n_checks, lay.edge_count
+        p, st = lay.plan().handle, _lib.stream_handle()
+        sigma = q.ebn0_to_sigma(2.6, 5 / 6)
+        mu = torch.empty((N, G), dtype=torch.float32, device="cuda")
+        _lib.call("qc_channel", 3, 0, 0, 0, N, G, sigma, mu.data_ptr(), None, None, st)
+        a = torch.zeros((E, G), dtype=torch.float32, device="cuda")
+        # iteration 1 (fused init) on both schedules
+        _lib.call("qc_cnu_ex", p, G, 1, a.data_ptr(), mu.data_ptr(), None, st)
+        _lib.call("qc_vnu_ex", p, G, 1, a.data_ptr(), mu.data_ptr(), None, None, None, st)
+        b = torch.zeros((E, G), dtype=torch.float32, device="cuda")
+        agg = torch.zeros((M, 3, G), dtype=torch.float32, device="cuda")
+        _lib.call("qc_agg_check", p, G, 1, b.data_ptr(), mu.data_ptr(), agg.data_ptr(), st)
+        _lib.call("qc_agg_var", p, G, 1, b.data_ptr(), mu.data_ptr(), agg.data_ptr(), None, None, st)
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32)), name
+        for _ in range(3):       # middle iterations
+            _lib.call("qc_cnu_ex", p, G, 2, a.data_ptr(), mu.data_ptr(), None, st)
+            _lib.call("qc_vnu_ex", p, G, 1, a.data_ptr(), mu.data_ptr(), None, None, None, st)
+            _lib.call("qc_agg_check", p, G, 0, b.data_ptr(), mu.data_ptr(), agg.data_ptr(), st)
+            _lib.call("qc_agg_var", p, G, 0, b.data_ptr(), mu.data_ptr(), agg.data_ptr(), None, None, st)
+            assert torch.equal(a.view(torch.int32), b.view(torch.int32)), name
+        pa = torch.zeros((N, G), dtype=torch.float32, device="cuda")
+        pb = torch.zeros_like(pa)
+        ha = torch.zeros((N, G // 32), dtype=torch.int32, device="cuda")
+        hb = torch.zeros_like(ha)
+        _lib.call("qc_cnu_ex", p, G, 2, a.data_ptr(), mu.data_ptr(), None, st)
+        _lib.call("qc_vnu_ex", p, G, 2, a.data_ptr(), mu.data_ptr(), pa.data_ptr(), ha.data_ptr(), None, st)
+        _lib.call("qc_agg_check", p, G, 0, b.data_ptr(), mu.data_ptr(), agg.data_ptr(), st)
+        _lib.call("qc_agg_var", p, G, 2, b.data_ptr(), mu.data_ptr(), agg.data_ptr(), pb.data_ptr(),
+                  hb.data_ptr(), st)
+        assert torch.equal(pa.view(torch.int32), pb.view(torch.int32)) and torch.equal(ha, hb), name
+
+
+_AGG_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+import paper_1204_0334_b200 as q
+h, exp = q.load_code(q.codes.bundled_code_path('n18360'))
+lay = q.build_edge_layout(h)
+y = q.simulate_block(q.ChannelConfig(2.9, 5 / 6, seed=5, gamma=int(sys.argv[2])), lay.n_vars)
+r = q.decode_batch(lay, y, q.ebn0_to_sigma(2.9, 5 / 6), 30)
+np.save(sys.argv[1], r.posteriors)
+"""
+
+
+def test_compact_schedule_decode_is_bit_identical(gpu, tmp_path):
+    """QCB_AGG=0 (two-pass schedule) and the default compact schedule decode the
+    same batch to bit-identical posteriors, for several lane-group sizes."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for gamma in (384, 512):      # 512: fused half-iteration kernels; 384: unfused compact passes
+        outs = []
+        for env in ({"QCB_AGG": "0"}, {"QCB_AGG": "1"}, {"QCB_AGG_LG": "128", "QCB_AGG_REV": "0"},
+                    {"QCB_AGG_FUSED": "0"}, {"QCB_AGG_FVC": "4"}, {"QCB_AGG_TILE": "256"}):
+            f = tmp_path / f"post{gamma}_{len(outs)}.npy"
+            subprocess.run([sys.executable, "-c", _AGG_SNIPPET, str(f), str(gamma)], cwd=repo, check=True,
+                           env={**os.environ, **env})
+            outs.append(np.load(f))
+        for o in outs[1:]:
+            assert np.array_equal(outs[0], o), gamma

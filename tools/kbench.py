@@ -54,6 +54,22 @@ def main():
         cnu_mu = timeit(lambda: _lib.call("qc_cnu_ex", p, G, 1, dec.msgs.data_ptr(), dec.mu.data_ptr(), None, st))
         vnu_phi = timeit(lambda: _lib.call("qc_vnu_ex", p, G, 1, dec.msgs.data_ptr(), dec.mu.data_ptr(), None,
                                            None, None, st))
+        agg_ms = {}
+        W = G // 32
+        agg_ptr = dec.work.data_ptr() + ((2 * W + 4 + 63) // 64 * 64) * 4
+        if os.environ.get("QCB_AGG", "1") != "0" and lay.check_regular:
+            agg_ms["agg_check_ms"] = timeit(lambda: _lib.call("qc_agg_check", p, G, 0, dec.msgs.data_ptr(),
+                                                              dec.mu.data_ptr(), agg_ptr, st))
+            agg_ms["agg_var_ms"] = timeit(lambda: _lib.call("qc_agg_var", p, G, 0, dec.msgs.data_ptr(),
+                                                            dec.mu.data_ptr(), agg_ptr, None, None, st))
+            if G % 256 == 0 and os.environ.get("QCB_AGG_FUSED", "1") != "0":
+                H = G // 2
+                agg_ms["agg_fused_half_ms"] = timeit(lambda: _lib.call(
+                    "qc_agg_fused", p, G, H, 0, 0, H, 0, dec.msgs.data_ptr(), dec.mu.data_ptr(), agg_ptr,
+                    None, None, st))
+            M = lay.n_checks
+            agg_ms["agg_check_gbs"] = (E + 3 * M) * G * 4 / agg_ms["agg_check_ms"] / 1e6
+            agg_ms["agg_var_gbs"] = (2 * E + N + 3 * M) * G * 4 / agg_ms["agg_var_ms"] / 1e6
         dec_ms = timeit(dec.run, max(3, args.reps // 4))
         mean_it = float(dec.iters[:G].float().mean().item())
         cb, vb = 2 * E * G * 4, (2 * E + N) * G * 4
@@ -66,6 +82,9 @@ def main():
             "decode_ms": round(dec_ms, 3), "decode_alg_gbs": round(alg / dec_ms / 1e6, 1),
             "decode_frac": round(alg / dec_ms / 1e6 / peak, 4),
             "mbit_s": round(G * (N - lay.n_checks) / dec_ms / 1e3, 1),
+            **{k: round(v, 4) for k, v in agg_ms.items()},
+            "agg_env": os.environ.get("QCB_AGG", "1"), "agg_lg": os.environ.get("QCB_AGG_LG", "512"),
+            "fused": os.environ.get("QCB_AGG_FUSED", "1"), "fvc": os.environ.get("QCB_AGG_FVC", "2"), "vv": os.environ.get("QCB_AGG_VV", "4"),
             "early_stop": args.early_stop, "ebn0_db": args.ebn0, "mean_iterations": round(mean_it, 2)}), flush=True)
         del dec
         torch.cuda.empty_cache()
