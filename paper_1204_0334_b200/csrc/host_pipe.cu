@@ -10,7 +10,7 @@
 //      + hard decision + syndrome) -> lane-major fp64 posteriors + u8 bits
 //   -> D2H of posteriors, bits, syndrome flags, iteration counts.
 // While one chunk decodes, the next is copied in and the previous one is read
-// back, so PCIe (55 GB/s each way on the B200 box, profiles/r02/pcie.json)
+// back, so PCIe (55 GB/s each way on the B200 box, profiles/r01/pcie.json)
 // overlaps the kernels.  Host arrays that are page-locked (cudaHostAlloc /
 // torch pin_memory / cudaHostRegister) are DMA'd in place; pageable arrays go
 // through per-slot pinned staging with a multi-threaded memcpy.
