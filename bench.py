@@ -16,9 +16,12 @@ reads posteriors (fp64) + hard bits (u8) + syndrome flags + iteration counts
 back (native chunked pipeline, csrc/host_pipe.cu); `pageable_input_value` is
 the same with y in ordinary pageable memory.
 
-`roofline` = the check-node kernel (the dominant launch): algorithmic bytes per
-launch (read + write of E x gamma fp32 packages) / its CUDA-event-timed
-duration, against the measured HBM copy bandwidth in MEASURED_PEAKS.json.
+`roofline` = the dominant launch, the fused half-iteration kernel of the
+compact check-state schedule: its compulsory bytes per
+launch (4 (3E + N + 6M) per lane of the half) / its CUDA-event-timed duration,
+against the measured HBM copy bandwidth in MEASURED_PEAKS.json;
+`ref_schedule` restates the same time in the reference schedule's bytes
+(4 (4E + N) per lane-iteration), which the compact schedule beats.
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port of qcldpc.bp, numpy float64) on all host cores.
@@ -226,9 +229,10 @@ def stream_bench(args, q, rank, W, group, barrier):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--gamma", type=int, default=4096)
+    ap.add_argument("--gamma", type=int, default=1024, help="lanes per step (kernel batch)")
+    ap.add_argument("--e2e-gamma", type=int, default=4096, help="lanes per decode_batch call of the e2e leg")
     ap.add_argument("--stream-gamma", type=int, default=512, help="lanes of the LDPCCC measurement (0 = skip)")
     ap.add_argument("--stream-steps", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -287,49 +291,64 @@ def main():
     value = frames * K_info / (ms / 1e3) / 1e6
     counts = eng.counts.cpu().numpy()
 
-    # ---- dominant kernel: check-node pass, CUDA events on the launching stream ----
+    # ---- dominant kernel: the fused half-iteration kernel of the compact
+    # schedule (variable job on one lane half + check job on the other; 2 x 30 - 1
+    # of the decode's launches), CUDA events on the launching stream ----
     dec = eng.dec
     st = _lib.stream_handle()
     reps = 20
-    for _ in range(3):
-        _lib.call("qc_cnu_ex", dec.plan.handle, dec.gp, 2, dec.msgs.data_ptr(), dec.mu.data_ptr(), None, st)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        _lib.call("qc_cnu_ex", dec.plan.handle, dec.gp, 2, dec.msgs.data_ptr(), dec.mu.data_ptr(), None, st)
-    e1.record()
-    torch.cuda.synchronize()
-    cnu_ms = e0.elapsed_time(e1) / reps
-    e0.record()
-    for _ in range(reps):
-        _lib.call("qc_vnu_ex", dec.plan.handle, dec.gp, 1, dec.msgs.data_ptr(), dec.mu.data_ptr(), None,
-                  None, None, st)
-    e1.record()
-    torch.cuda.synchronize()
-    vnu_ms = e0.elapsed_time(e1) / reps
-    cnu_bytes = 2 * E * gamma * 4
-    vnu_bytes = (2 * E + N) * gamma * 4
+    H = gamma // 2
+    W32 = gamma // 32
+    agg_ptr = dec.work.data_ptr() + ((2 * W32 + 4 + 63) // 64 * 64) * 4    # records region (qc_decode_work_words)
+    fused = lambda: _lib.call("qc_agg_fused", dec.plan.handle, gamma, H, 0, 0, H, 0, dec.msgs.data_ptr(),
+                              dec.mu.data_ptr(), agg_ptr, None, None, st)
+    check = lambda: _lib.call("qc_agg_check", dec.plan.handle, gamma, 0, dec.msgs.data_ptr(), dec.mu.data_ptr(),
+                              agg_ptr, st)
+
+    def ev_ms(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    fused_ms, check_ms = ev_ms(fused), ev_ms(check)
     peak, peak_kind = load_peaks()
+    # compulsory bytes of the compact schedule, per lane and iteration:
+    # check job reads E packages, writes 3M record words; variable job reads E
+    # packages + N LLRs + 3M record words once, writes E packages
+    fused_bytes = 4 * (3 * E + N + 6 * M) * H
+    ref_bytes = 4 * (4 * E + N) * H             # the reference schedule's bytes for the same work
+    check_bytes = 4 * (E + 3 * M) * gamma
+    fach = fused_bytes / (fused_ms / 1e3) / 1e9
     step_alg = algorithmic_bytes_per_codeword(E, N, ITERS) * gamma
-    # dominant kernel by share of the step (ncu launch list, profiles/r01/launch_share_bench.md):
-    # the variable pass (47.6%) just ahead of the check pass (44.8%)
-    vach = vnu_bytes / (vnu_ms / 1e3) / 1e9
-    cach = cnu_bytes / (cnu_ms / 1e3) / 1e9
-    tv, tc = ncu_traffic("vnu_phi", gamma), ncu_traffic("cnu_phi", gamma)
-    roofline = {"bound": "hbm", "achieved": round(vach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(vach / peak, 4),
-                "traffic": int(tv["dram_bytes"]) if tv else None,
-                "kernel": "vnu_kernel<4,4,QC,VNU_PHI> (variable pass, phi form; 29 of 30 iterations)",
-                "peak_kind": peak_kind, "bytes_per_launch": vnu_bytes, "launch_ms": round(vnu_ms, 4),
-                "traffic_source": (tv or {}).get("source"),
-                "check_pass": {"kernel": "cnu_kernel<24,2,REG,CNU_PHI>", "achieved": round(cach, 1),
-                               "frac": round(cach / peak, 4), "launch_ms": round(cnu_ms, 4),
-                               "bytes_per_launch": cnu_bytes,
-                               "traffic": int(tc["dram_bytes"]) if tc else None},
-                "step": {"alg_bytes": step_alg,
-                         "achieved": round(step_alg / (ms / args.steps / 1e3) / 1e9, 1),
-                         "frac": round(step_alg / (ms / args.steps / 1e3) / 1e9 / peak, 4)}}
+    tf = ncu_traffic("agg_fused", gamma)
+    roofline = {"bound": "hbm", "achieved": round(fach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(fach / peak, 4),
+                "traffic": int(tf["dram_bytes"]) if tf else None,
+                "kernel": "agg_fused_kernel<24,4,2,4,0,0> (variable job + check job, compact schedule; "
+                          "59 of 65 launches of a 30-iteration decode)",
+                "peak_kind": peak_kind, "bytes_per_launch": fused_bytes, "launch_ms": round(fused_ms, 4),
+                "traffic_source": (tf or {}).get("source"),
+                "ref_schedule": {"bytes_per_launch": ref_bytes,
+                                 "equiv_GBs": round(ref_bytes / (fused_ms / 1e3) / 1e9, 1),
+                                 "equiv_frac": round(ref_bytes / (fused_ms / 1e3) / 1e9 / peak, 4)},
+                "check_pass": {"kernel": "agg_check_kernel<24,4,0> (records only)",
+                               "achieved": round(check_bytes / (check_ms / 1e3) / 1e9, 1),
+                               "frac": round(check_bytes / (check_ms / 1e3) / 1e9 / peak, 4),
+                               "launch_ms": round(check_ms, 4), "bytes_per_launch": check_bytes},
+                "step": {"ref_schedule_alg_bytes": step_alg,
+                         "ref_schedule_equiv_GBs": round(step_alg / (ms / args.steps / 1e3) / 1e9, 1),
+                         "ref_schedule_equiv_frac": round(step_alg / (ms / args.steps / 1e3) / 1e9 / peak, 4),
+                         "compact_alg_bytes": 4 * ITERS * (3 * E + N + 6 * M) * gamma,
+                         "compact_frac": round(4 * ITERS * (3 * E + N + 6 * M) * gamma /
+                                               (ms / args.steps / 1e3) / 1e9 / peak, 4)}}
+    del check
 
     # ---- e2e through the public API with host buffers ----
     # decode_batch(layout, y, sigma, 30) with y (gamma, N) fp64 in page-locked
@@ -341,7 +360,8 @@ def main():
     if not args.no_e2e:
         import numpy as np
         rng = np.random.default_rng(rank)
-        y_pageable = 1.0 + sigma * rng.standard_normal((gamma, N))
+        GE = args.e2e_gamma
+        y_pageable = 1.0 + sigma * rng.standard_normal((GE, N))
         y = q.host_array(y_pageable)
 
         def e2e_rate(yin, steps):
@@ -356,12 +376,13 @@ def main():
                 del r
             barrier()
             dt = max_scalar(time.perf_counter() - t0, group, device="cuda")
-            return round(steps * gamma * W * K_info / dt / 1e6, 2)
+            return round(steps * GE * W * K_info / dt / 1e6, 2)
 
         e_steps = max(3, args.steps // 2)
         e2e = {"value": e2e_rate(y, e_steps), "unit": "Mbit/s",
-               "h2d_bytes_per_step": gamma * N * 8,
-               "d2h_bytes_per_step": gamma * N * 8 + gamma * N + gamma + gamma * 4,
+               "h2d_bytes_per_step": GE * N * 8,
+               "d2h_bytes_per_step": GE * N * 8 + GE * N + GE + GE * 8,
+               "lanes_per_step": GE,
                "api": "paper_1204_0334_b200.decode_batch (numpy y in page-locked host memory; "
                       "DecodeResult out: fp64 posteriors, u8 bits, ok, iterations)",
                "steps": e_steps,

@@ -146,6 +146,8 @@ typedef struct qc_host_dec qc_host_dec;
 QC_API int qc_host_create(const qc_plan* plan, int chunk, int slots, int iters, int early_stop,
                           qc_host_dec** out);
 QC_API void qc_host_destroy(qc_host_dec* dec);
+/* 1 if [p, p + bytes) is page-locked host memory (DMA'd in place), else 0 */
+QC_API int qc_host_is_pinned(const void* p, size_t bytes);
 /* dims: chunk, slots, iters, early_stop, device */
 QC_API int qc_host_dims(const qc_host_dec* dec, int64_t* dims);
 QC_API int qc_host_decode(qc_host_dec* dec, const double* x, int gamma, double sigma, uint8_t* bits,

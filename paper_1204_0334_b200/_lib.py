@@ -49,6 +49,7 @@ SIGNATURES = {
     "qc_host_create": (_i, [_p, _i, _i, _i, _i, C.POINTER(_p)]),
     "qc_host_destroy": (None, [_p]),
     "qc_host_dims": (_i, [_p, _p]),
+    "qc_host_is_pinned": (_i, [_p, C.c_size_t]),
     "qc_host_decode": (_i, [_p, _p, _i, _d, _p, _p, _p, _p]),
     "qc_rc_state_bytes": (C.c_size_t, [_i]),
     "qc_rc_init": (_i, [_i, _i64, _p, _p]),

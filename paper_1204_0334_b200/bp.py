@@ -318,7 +318,8 @@ class BlockDecoder:
 
 
 HOST_CHUNK = 256        # lanes per pipelined chunk of the host-buffer API (tools/e2e_bench.py)
-HOST_SLOTS = 4          # CUDA streams (device buffer sets) the chunks rotate over
+HOST_SLOTS = 4          # CUDA streams (device buffer sets) the chunks rotate over, pageable input
+HOST_SLOTS_PINNED = 3   # same for page-locked input (no host staging copy to hide; tools/e2e_bench.py)
 PINNED_MIN_BYTES = 1 << 20
 
 
@@ -376,10 +377,11 @@ def host_array(a: np.ndarray) -> np.ndarray:
     return out
 
 
-def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool) -> HostDecoder:
+def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool,
+                  pinned_input: bool = False) -> HostDecoder:
     import torch
     chunk = min(HOST_CHUNK, pad32(gamma))
-    slots = HOST_SLOTS if gamma > chunk else 1
+    slots = (HOST_SLOTS_PINNED if pinned_input else HOST_SLOTS) if gamma > chunk else 1
     cache = layout.__dict__.setdefault("_host_decoders", {})
     key = (chunk, slots, iterations, bool(early_stop), torch.cuda.current_device())
     dec = cache.get(key)
@@ -413,7 +415,9 @@ def _decode_host(layout: EdgeLayout, x: np.ndarray, sigma: float | None, iterati
         dec.load_lane_major(x, sigma)
         dec.run()
         return dec.result(x.shape[0])
-    return _host_decoder(layout, x.shape[0], iterations, early_stop).decode(x, sigma or 0.0)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    pinned = bool(x.size) and _lib.load().qc_host_is_pinned(x.ctypes.data, x.nbytes) == 1
+    return _host_decoder(layout, x.shape[0], iterations, early_stop, pinned).decode(x, sigma or 0.0)
 
 
 def decode_llr_batch(layout: EdgeLayout, mu: np.ndarray, iterations: int,

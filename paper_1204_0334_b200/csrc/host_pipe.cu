@@ -202,6 +202,8 @@ void qc_host_destroy(qc_host_dec* h) {
   delete h;
 }
 
+int qc_host_is_pinned(const void* p, size_t bytes) { return pinned(p, bytes) ? 1 : 0; }
+
 int qc_host_dims(const qc_host_dec* h, int64_t* dims) {
   if (!h || !dims) return fail_arg("null argument");
   dims[0] = h->chunk;
