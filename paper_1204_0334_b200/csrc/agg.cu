@@ -39,6 +39,7 @@ struct AggArgs {
   int lg_gw;           // log2(lane vectors per group)
   int groups;          // lane groups in the window
   int reverse;         // visit lane groups last-to-first
+  int rows_eff;        // rows the grid covers (rows / items per thread, rounded up)
 };
 
 // min CTAs/SM for the variable job: 4 x 256 threads caps it at 64 registers,
@@ -55,7 +56,7 @@ enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
 __device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned grp, int& row, int& q) {
   const unsigned idx = bx * THREADS + threadIdx.x;
   row = (int)(idx >> a.lg_gw);
-  if (row >= a.rows) return false;
+  if (row >= a.rows_eff) return false;
   const int g = a.reverse ? a.groups - 1 - (int)grp : (int)grp;
   q = a.q0 + (g << a.lg_gw) + (int)(idx & ((1u << a.lg_gw) - 1u));
   return true;
@@ -183,6 +184,36 @@ __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, i
   }
 }
 
+// L2 prefetch of an item's HBM operands (its LLR row and d_v packages); the
+// check records are L2-resident already
+template <int DV, int VEC, int FLAGS>
+__device__ __forceinline__ void var_prefetch(const AggArgs& a, const QcGrid& grid, int n, int q) {
+  const int l = div_p(grid, n), c = n - l * grid.p;
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a.mu + (size_t)n * a.gamma + q * VEC));
+  if constexpr (!(FLAGS & AGG_FIRST)) {
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      int rr = c - grid.s[j * grid.L + l];
+      rr += (rr < 0) ? grid.p : 0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.msgs + ((size_t)(j * grid.p + rr) * grid.L + l) * a.gamma +
+                                                       q * VEC));
+    }
+  }
+}
+
+// ITEMS rows per thread (n, n + rows_eff, ...): the next item's operands are
+// prefetched into L2 before the current one's arithmetic
+template <int DV, int VEC, int FLAGS, int ITEMS>
+__device__ __forceinline__ void var_items(const AggArgs& a, const QcGrid& grid, int n, int q) {
+#pragma unroll 1
+  for (int k = 0; k < ITEMS; ++k) {
+    const int nk = n + k * a.rows_eff;
+    if (nk >= a.rows) break;                                   // warp-uniform (one row per warp)
+    if (k + 1 < ITEMS && nk + a.rows_eff < a.rows) var_prefetch<DV, VEC, FLAGS>(a, grid, nk + a.rows_eff, q);
+    var_body<DV, VEC, FLAGS>(a, grid, nk, q);
+  }
+}
+
 // grid = (blocks per lane group, groups)
 template <int DC, int VEC, bool FROM_MU>
 __global__ void __launch_bounds__(THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
@@ -190,10 +221,10 @@ __global__ void __launch_bounds__(THREADS) agg_check_kernel(AggArgs a, const __g
   if (agg_map(a, blockIdx.x, blockIdx.y, m, q)) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
 }
 
-template <int DV, int VEC, int FLAGS>
+template <int DV, int VEC, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   int n, q;
-  if (agg_map(a, blockIdx.x, blockIdx.y, n, q)) var_body<DV, VEC, FLAGS>(a, grid, n, q);
+  if (agg_map(a, blockIdx.x, blockIdx.y, n, q)) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
 }
 
 // One launch, two independent jobs on disjoint lane windows: the variable pass
@@ -212,7 +243,7 @@ __device__ __forceinline__ unsigned div_magic(unsigned x, unsigned long long m) 
   return (unsigned)(((unsigned long long)x * m) >> 40);
 }
 
-template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS>
+template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
   int row, q;
   if (blockIdx.x == f.R) {
@@ -222,7 +253,7 @@ __global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedA
     const unsigned b = blockIdx.y * f.R + blockIdx.x;
     if (b >= f.nbv) return;
     const unsigned g = div_magic(b, f.v_magic);
-    if (agg_map(f.v, b - g * f.v_bpg, g, row, q)) var_body<DV, VV, FLAGS>(f.v, grid, row, q);
+    if (agg_map(f.v, b - g * f.v_bpg, g, row, q)) var_items<DV, VV, FLAGS, ITEMS>(f.v, grid, row, q);
   }
 }
 
@@ -257,6 +288,10 @@ int agg_vv() {
   static int v = env_int("QCB_AGG_VV", 4);       // lanes per thread of the variable job (4 or 2)
   return v == 2 ? 2 : 4;
 }
+int agg_items() {
+  static int v = env_int("QCB_AGG_ITEMS", 2);    // rows per variable thread (2: L2 prefetch of the next; +1.5%)
+  return v == 2 ? 2 : 1;
+}
 int agg_fused_vc() {
   static int v = env_int("QCB_AGG_FVC", 2);      // lanes per thread of the fused check job
   return v == 4 ? 4 : 2;
@@ -277,7 +312,7 @@ int pick_lg_gw(int gamma, int vec) {
 }
 
 unsigned blocks_per_group(const AggArgs& a) {
-  return (unsigned)((((long long)a.rows << a.lg_gw) + THREADS - 1) / THREADS);
+  return (unsigned)((((long long)a.rows_eff << a.lg_gw) + THREADS - 1) / THREADS);
 }
 
 dim3 agg_grid(const AggArgs& a, int) { return dim3(blocks_per_group(a), (unsigned)a.groups, 1); }
@@ -285,7 +320,7 @@ dim3 agg_grid(const AggArgs& a, int) { return dim3(blocks_per_group(a), (unsigne
 // pass arguments over the lane window [lane0, lane0 + lanes) of a gamma-wide store
 AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_t* hb, int rows, int gamma,
                   int lane0, int lanes, int vec, int reverse) {
-  AggArgs a{msgs, mu, agg, post, hb, rows, gamma, lane0 / vec, pick_lg_gw(lanes, vec), 0, reverse};
+  AggArgs a{msgs, mu, agg, post, hb, rows, gamma, lane0 / vec, pick_lg_gw(lanes, vec), 0, reverse, rows};
   a.groups = (lanes / vec) >> a.lg_gw;
   return a;
 }
@@ -306,14 +341,24 @@ void launch_check_dc(const AggArgs& a, int vec, bool from_mu, const QcGrid& g, c
   }
 }
 
-template <int DV, int VEC>
-void launch_var_v(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
+template <int DV, int VEC, int ITEMS>
+void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
   switch (flags) {
-    case 0: agg_var_kernel<DV, VEC, 0><<<nb, THREADS, 0, s>>>(a, g); break;
-    case AGG_FIRST: agg_var_kernel<DV, VEC, AGG_FIRST><<<nb, THREADS, 0, s>>>(a, g); break;
-    case AGG_LAST: agg_var_kernel<DV, VEC, AGG_LAST><<<nb, THREADS, 0, s>>>(a, g); break;
-    default: agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST><<<nb, THREADS, 0, s>>>(a, g);
+    case 0: agg_var_kernel<DV, VEC, 0, ITEMS><<<nb, THREADS, 0, s>>>(a, g); break;
+    case AGG_FIRST: agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS><<<nb, THREADS, 0, s>>>(a, g); break;
+    case AGG_LAST: agg_var_kernel<DV, VEC, AGG_LAST, ITEMS><<<nb, THREADS, 0, s>>>(a, g); break;
+    default: agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS><<<nb, THREADS, 0, s>>>(a, g);
+  }
+}
+
+template <int DV, int VEC>
+void launch_var_v(AggArgs a, int flags, const QcGrid& g, cudaStream_t s) {
+  if (agg_items() == 2) {
+    a.rows_eff = (a.rows + 1) / 2;
+    launch_var_i<DV, VEC, 2>(a, flags, g, s);
+  } else {
+    launch_var_i<DV, VEC, 1>(a, flags, g, s);
   }
 }
 
@@ -328,8 +373,8 @@ void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaSt
 
 template <int DC, int DV, int VC, bool FROM_MU, int FLAGS>
 void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t s) {
-  if (agg_vv() == 2) agg_fused_kernel<DC, DV, VC, 2, FROM_MU, FLAGS><<<grid, THREADS, 0, s>>>(f, g);
-  else agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS><<<grid, THREADS, 0, s>>>(f, g);
+  if (agg_items() == 2) agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 2><<<grid, THREADS, 0, s>>>(f, g);
+  else agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 1><<<grid, THREADS, 0, s>>>(f, g);
 }
 
 template <int DC, int DV, int VC>
@@ -364,7 +409,8 @@ int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, 
                      const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s) {
   const int vc = agg_fused_vc();
   FusedArgs f;
-  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, agg_vv(), agg_reverse());
+  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, 4, agg_reverse());
+  if (agg_items() == 2) f.v.rows_eff = (f.v.rows + 1) / 2;
   f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, vc, 0);
   f.v_bpg = blocks_per_group(f.v);
   f.c_bpg = blocks_per_group(f.c);
