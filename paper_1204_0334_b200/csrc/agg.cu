@@ -45,8 +45,11 @@ struct AggArgs {
 // min CTAs/SM for the variable job: 4 x 256 threads caps it at 64 registers,
 // enough to issue all 17 loads of an item before its arithmetic (measured best
 // on B200: 2 -> 88 regs / 16 warps is 15% slower, 5 -> 48 regs spills)
+#ifndef AGG_THREADS
+#define AGG_THREADS 128   // 128 > 64, 256 (+2.5%), 512 (profiles/r01/kbench_compact_threads.jsonl)
+#endif
 #ifndef AGG_VAR_MINB
-#define AGG_VAR_MINB 4
+#define AGG_VAR_MINB (1024 / AGG_THREADS)
 #endif
 
 enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
@@ -54,7 +57,7 @@ enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
 // block (bx within its lane group, group index) + thread -> (row, lane vector q).
 // Lane-group major: every row of one group of lanes before the next group.
 __device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned grp, int& row, int& q) {
-  const unsigned idx = bx * THREADS + threadIdx.x;
+  const unsigned idx = bx * AGG_THREADS + threadIdx.x;
   row = (int)(idx >> a.lg_gw);
   if (row >= a.rows_eff) return false;
   const int g = a.reverse ? a.groups - 1 - (int)grp : (int)grp;
@@ -216,13 +219,13 @@ __device__ __forceinline__ void var_items(const AggArgs& a, const QcGrid& grid, 
 
 // grid = (blocks per lane group, groups)
 template <int DC, int VEC, bool FROM_MU>
-__global__ void __launch_bounds__(THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+__global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   int m, q;
   if (agg_map(a, blockIdx.x, blockIdx.y, m, q)) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
 }
 
 template <int DV, int VEC, int FLAGS, int ITEMS>
-__global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+__global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   int n, q;
   if (agg_map(a, blockIdx.x, blockIdx.y, n, q)) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
 }
@@ -244,7 +247,7 @@ __device__ __forceinline__ unsigned div_magic(unsigned x, unsigned long long m) 
 }
 
 template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
-__global__ void __launch_bounds__(THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
+__global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
   int row, q;
   if (blockIdx.x == f.R) {
     const unsigned b = blockIdx.y, g = div_magic(b, f.c_magic);
@@ -312,7 +315,7 @@ int pick_lg_gw(int gamma, int vec) {
 }
 
 unsigned blocks_per_group(const AggArgs& a) {
-  return (unsigned)((((long long)a.rows_eff << a.lg_gw) + THREADS - 1) / THREADS);
+  return (unsigned)((((long long)a.rows_eff << a.lg_gw) + AGG_THREADS - 1) / AGG_THREADS);
 }
 
 dim3 agg_grid(const AggArgs& a, int) { return dim3(blocks_per_group(a), (unsigned)a.groups, 1); }
@@ -328,8 +331,8 @@ AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_
 template <int DC, int VEC>
 void launch_check_v(const AggArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
-  if (from_mu) agg_check_kernel<DC, VEC, true><<<nb, THREADS, 0, s>>>(a, g);
-  else agg_check_kernel<DC, VEC, false><<<nb, THREADS, 0, s>>>(a, g);
+  if (from_mu) agg_check_kernel<DC, VEC, true><<<nb, AGG_THREADS, 0, s>>>(a, g);
+  else agg_check_kernel<DC, VEC, false><<<nb, AGG_THREADS, 0, s>>>(a, g);
 }
 
 template <int DC>
@@ -345,10 +348,10 @@ template <int DV, int VEC, int ITEMS>
 void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
   switch (flags) {
-    case 0: agg_var_kernel<DV, VEC, 0, ITEMS><<<nb, THREADS, 0, s>>>(a, g); break;
-    case AGG_FIRST: agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS><<<nb, THREADS, 0, s>>>(a, g); break;
-    case AGG_LAST: agg_var_kernel<DV, VEC, AGG_LAST, ITEMS><<<nb, THREADS, 0, s>>>(a, g); break;
-    default: agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS><<<nb, THREADS, 0, s>>>(a, g);
+    case 0: agg_var_kernel<DV, VEC, 0, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g); break;
+    case AGG_FIRST: agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g); break;
+    case AGG_LAST: agg_var_kernel<DV, VEC, AGG_LAST, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g); break;
+    default: agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g);
   }
 }
 
@@ -373,8 +376,8 @@ void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaSt
 
 template <int DC, int DV, int VC, bool FROM_MU, int FLAGS>
 void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t s) {
-  if (agg_items() == 2) agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 2><<<grid, THREADS, 0, s>>>(f, g);
-  else agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 1><<<grid, THREADS, 0, s>>>(f, g);
+  if (agg_items() == 2) agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 2><<<grid, AGG_THREADS, 0, s>>>(f, g);
+  else agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 1><<<grid, AGG_THREADS, 0, s>>>(f, g);
 }
 
 template <int DC, int DV, int VC>
