@@ -39,6 +39,9 @@
 
 using namespace qcb;
 
+#ifndef CC_THREADS
+#define CC_THREADS 128   // +0.8% over 256 (profiles/r01/sbench_threads.jsonl)
+#endif
 #define CC_MAX_LAM 8
 #define CC_MAX_SHIFTS 2048
 
@@ -173,7 +176,7 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
 // ---- entry: frame t into ring slot t mod window and its T sub-blocks --------
 // Also folds the previous slot's emitted-frame bit count into the lane counters.
 template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
-__global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+__global__ void __launch_bounds__(CC_THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC, window = P.I * T;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(THREADS) entry_kernel(SlotArgs a, const __grid
 // TT, WW > 0: period and sub-block width known at compile time (QC grids of the
 // common shapes) so the edge walk fully unrolls; 0 = runtime values.
 template <int DC, int VEC, bool QC, int TT = 0, int WW = 0>
-__global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+__global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(THREADS) check_kernel(SlotArgs a, const __grid
 
 // ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 ------
 template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
-__global__ void __launch_bounds__(THREADS) var_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+__global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -388,25 +391,25 @@ template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_entry(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
   long long n = (long long)P.c * (P.gamma / vec);
-  unsigned nb = blocks_for(std::max<long long>(n, P.gamma));
-  if (vec == 4) entry_kernel<DV, 4, QC, TT, SJ><<<nb, THREADS, 0, s>>>(a, P);
-  else if (vec == 2) entry_kernel<DV, 2, QC, TT, SJ><<<nb, THREADS, 0, s>>>(a, P);
-  else entry_kernel<DV, 1, QC, TT, SJ><<<nb, THREADS, 0, s>>>(a, P);
+  unsigned nb = blocks_for(std::max<long long>(n, P.gamma), CC_THREADS);
+  if (vec == 4) entry_kernel<DV, 4, QC, TT, SJ><<<nb, CC_THREADS, 0, s>>>(a, P);
+  else if (vec == 2) entry_kernel<DV, 2, QC, TT, SJ><<<nb, CC_THREADS, 0, s>>>(a, P);
+  else entry_kernel<DV, 1, QC, TT, SJ><<<nb, CC_THREADS, 0, s>>>(a, P);
 }
 template <int DC, bool QC, int TT = 0, int WW = 0>
 void launch_check(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, DC > 24 ? 1 : 2);
   long long n = (long long)P.I * P.cb * (P.gamma / vec);
-  if (vec == 2) check_kernel<DC, 2, QC, TT, WW><<<blocks_for(n), THREADS, 0, s>>>(a, P);
-  else check_kernel<DC, 1, QC, TT, WW><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  if (vec == 2) check_kernel<DC, 2, QC, TT, WW><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
+  else check_kernel<DC, 1, QC, TT, WW><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
 }
 template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_var(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
   long long n = (long long)P.I * P.c * (P.gamma / vec);
-  if (vec == 4) var_kernel<DV, 4, QC, TT, SJ><<<blocks_for(n), THREADS, 0, s>>>(a, P);
-  else if (vec == 2) var_kernel<DV, 2, QC, TT, SJ><<<blocks_for(n), THREADS, 0, s>>>(a, P);
-  else var_kernel<DV, 1, QC, TT, SJ><<<blocks_for(n), THREADS, 0, s>>>(a, P);
+  if (vec == 4) var_kernel<DV, 4, QC, TT, SJ><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
+  else if (vec == 2) var_kernel<DV, 2, QC, TT, SJ><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
+  else var_kernel<DV, 1, QC, TT, SJ><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
 }
 
 template <int DV, bool QC>
@@ -562,7 +565,7 @@ int cc_slot(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev
 
 int cc_fold(int32_t* lane_cnt, int gamma, void* stream) {
   if (!lane_cnt || gamma <= 0) return fail_arg("bad fold arguments");
-  fold_kernel<<<blocks_for(gamma), THREADS, 0, as_stream(stream)>>>(lane_cnt, gamma);
+  fold_kernel<<<blocks_for(gamma, CC_THREADS), CC_THREADS, 0, as_stream(stream)>>>(lane_cnt, gamma);
   return check_launch("cc_fold");
 }
 
