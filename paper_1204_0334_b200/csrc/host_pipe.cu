@@ -2,9 +2,16 @@
 // (/root/reference/pkg/src/qcldpc/bp.py:213-274) with caller-owned HOST arrays,
 // lane-major in and out exactly as DecodeResult (bp.py:87-100).
 //
-// A batch of gamma codewords is cut into chunks of `chunk` lanes that rotate
-// over `slots` CUDA streams, each with its own device buffers and an
-// instantiated CUDA graph of the whole flooding loop (qc_decode).  Per chunk:
+// A batch of gamma codewords is cut into chunks that rotate over `slots` CUDA
+// streams, each with its own device buffers and instantiated CUDA graphs of
+// the whole flooding loop (qc_decode) for chunk sizes C/4, C/2 and C lanes
+// (C = `chunk`).  The chunk plan ramps C/4, C/2, C, ..., C, C/4: small first
+// and last chunks shorten the pipeline fill (first copy-in) and drain (last
+// copy-out), full-size chunks in between keep the decode kernels at their
+// large-gamma efficiency.  Decodes are serialised across streams (event
+// chain): two decodes running concurrently interfere (tools/chain_probe.py);
+// copy-ins are serialised too, so the first chunk is not slowed by later ones
+// sharing the link; copies in both directions overlap the decodes.  Per chunk:
 //   H2D of the received values (fp64, lane-major)
 //   -> LLR scale/clip/transpose kernel -> graph (init + iters x (check, variable)
 //      + hard decision + syndrome) -> lane-major fp64 posteriors + u8 bits
@@ -32,7 +39,10 @@ using namespace qcb;
 struct Slot {
   cudaStream_t st = nullptr;
   cudaEvent_t done = nullptr;
-  cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};   // C/4, C/2, C lanes
+  int size[3] = {0, 0, 0};
+  cudaEvent_t decoded = nullptr;   // end of this slot's last decode (serialises decodes)
+  cudaEvent_t copied_in = nullptr; // end of this slot's last copy-in (serialises copy-ins)
   double* x = nullptr;          // (chunk, N) fp64 lane-major input
   float* mu = nullptr;          // (N, chunk) fp32 LLRs
   float* msgs = nullptr;        // (E, chunk) packages
@@ -115,8 +125,11 @@ struct qc_host_dec {
 };
 
 static void free_slot(Slot& s) {
-  if (s.graph) cudaGraphExecDestroy(s.graph);
+  for (auto& g : s.graph)
+    if (g) cudaGraphExecDestroy(g);
   if (s.done) cudaEventDestroy(s.done);
+  if (s.decoded) cudaEventDestroy(s.decoded);
+  if (s.copied_in) cudaEventDestroy(s.copied_in);
   if (s.st) cudaStreamDestroy(s.st);
   void* dev[] = {s.x, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, s.post_lm, s.bits_lm};
   for (void* d : dev)
@@ -144,21 +157,29 @@ static int init_slot(qc_host_dec* h, Slot& s) {
   HP_CK(cudaMalloc(&s.bits_lm, C * N));
   HP_CK(cudaMallocHost(&s.h_ok, C));
   HP_CK(cudaMallocHost(&s.h_its, C * sizeof(int32_t)));
+  HP_CK(cudaEventCreateWithFlags(&s.decoded, cudaEventDisableTiming));
+  HP_CK(cudaEventCreateWithFlags(&s.copied_in, cudaEventDisableTiming));
   HP_CK(cudaMemsetAsync(s.msgs, 0, E * C * sizeof(float), s.st));
-  // the flooding loop, captured once: replayed per chunk
-  cudaGraph_t g = nullptr;
-  HP_CK(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
-  int rc = qc_decode(p, h->chunk, h->iters, h->early_stop, s.mu, s.msgs, s.post, s.hb, s.work, s.ok,
-                     s.its, nullptr, s.st);
-  cudaError_t ce = cudaStreamEndCapture(s.st, &g);
-  if (rc) {
-    if (g) cudaGraphDestroy(g);
-    return rc;
+  // the flooding loop for each chunk size, captured once and replayed per chunk
+  // (a size-c decode uses the slot's buffers with row stride c)
+  for (int i = 0; i < 3; ++i) {
+    const int c = h->chunk >> (2 - i);
+    if (c < 32 || c % 32) continue;
+    s.size[i] = c;
+    cudaGraph_t g = nullptr;
+    HP_CK(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
+    int rc = qc_decode(p, c, h->iters, h->early_stop, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, nullptr,
+                       s.st);
+    cudaError_t ce = cudaStreamEndCapture(s.st, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail_rt(std::string("graph capture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&s.graph[i], g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail_rt(std::string("graph instantiate: ") + cudaGetErrorString(ce));
   }
-  if (ce != cudaSuccess) return fail_rt(std::string("graph capture: ") + cudaGetErrorString(ce));
-  ce = cudaGraphInstantiate(&s.graph, g, 0);
-  cudaGraphDestroy(g);
-  if (ce != cudaSuccess) return fail_rt(std::string("graph instantiate: ") + cudaGetErrorString(ce));
   HP_CK(cudaStreamSynchronize(s.st));
   return 0;
 }
@@ -252,29 +273,66 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
          pinned(bits, (size_t)gamma * row)};
   const bool pin_in = pinned(x, (size_t)gamma * row * sizeof(double));
   const int S = (int)h->slots.size();
-  const long long nchunks = (gamma + h->chunk - 1) / h->chunk;
-  const size_t C = h->chunk;
+  const int C = h->chunk;
+  // chunk plan: C/4, C/2, C, ..., C, then the remainder and a final C/4
+  std::vector<int> plan;
+  long long rem = gamma;
+  if (gamma <= C) {
+    plan.push_back(gamma);
+    rem = 0;
+  }
+  for (int c : {C / 4, C / 2})
+    if (c >= 32 && c % 32 == 0 && rem > c + C / 4) {
+      plan.push_back(c);
+      rem -= c;
+    }
+  while (rem > C + C / 4) {
+    plan.push_back(C);
+    rem -= C;
+  }
+  if (rem > C / 4 && C / 4 >= 32 && C % 128 == 0 && !plan.empty()) {
+    plan.push_back((int)(rem - C / 4));
+    plan.push_back(C / 4);
+  } else {
+    while (rem > 0) {
+      const int c = (int)std::min<long long>(rem, C);
+      plan.push_back(c);
+      rem -= c;
+    }
+  }
+  const long long nchunks = (long long)plan.size();
+  cudaEvent_t prev_decoded = nullptr, prev_copied = nullptr;
+  long long a = 0;
   for (long long k = 0; k < nchunks; ++k) {
     Slot& s = h->slots[k % S];
     if (int rc = finish(c, s)) return rc;
-    const long long a = k * h->chunk, b = std::min<long long>(gamma, a + h->chunk);
-    const int gi = (int)(b - a);
+    const long long b = a + plan[k];
+    const int gi = plan[k];
+    int gsel = 2;                                   // smallest captured size holding the chunk
+    while (gsel > 0 && s.size[gsel - 1] >= gi) --gsel;
+    const int cs = s.size[gsel];
     const double* src = x + (size_t)a * row;
     if (!pin_in) {
-      if (!s.h_in) HP_CK(cudaMallocHost(&s.h_in, C * row * sizeof(double)));
+      if (!s.h_in) HP_CK(cudaMallocHost(&s.h_in, (size_t)C * row * sizeof(double)));
       par_copy(s.h_in, src, (size_t)gi * row * sizeof(double));
       src = s.h_in;
     }
+    // copy-ins in chunk order, one at a time: the first chunk gets the whole link
+    if (prev_copied) HP_CK(cudaStreamWaitEvent(s.st, prev_copied, 0));
     HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
-    if (int rc = qc_llr_from_lane_major(N, h->chunk, gi, s.x, sigma, s.mu, s.st)) return rc;
-    HP_CK(cudaGraphLaunch(s.graph, s.st));
-    if (int rc = qc_lane_major(N, h->chunk, gi, s.post, post ? s.post_lm : nullptr,
-                               bits ? s.bits_lm : nullptr, s.st))
+    HP_CK(cudaEventRecord(s.copied_in, s.st));
+    prev_copied = s.copied_in;
+    if (prev_decoded) HP_CK(cudaStreamWaitEvent(s.st, prev_decoded, 0));
+    if (int rc = qc_llr_from_lane_major(N, cs, gi, s.x, sigma, s.mu, s.st)) return rc;
+    HP_CK(cudaGraphLaunch(s.graph[gsel], s.st));
+    HP_CK(cudaEventRecord(s.decoded, s.st));
+    prev_decoded = s.decoded;
+    if (int rc = qc_lane_major(N, cs, gi, s.post, post ? s.post_lm : nullptr, bits ? s.bits_lm : nullptr, s.st))
       return rc;
     if (post) {
       double* dst = c.pin_post ? post + (size_t)a * row : nullptr;
       if (!dst) {
-        if (!s.h_post) HP_CK(cudaMallocHost(&s.h_post, C * row * sizeof(double)));
+        if (!s.h_post) HP_CK(cudaMallocHost(&s.h_post, (size_t)C * row * sizeof(double)));
         dst = s.h_post;
       }
       HP_CK(cudaMemcpyAsync(dst, s.post_lm, (size_t)gi * row * sizeof(double), cudaMemcpyDeviceToHost, s.st));
@@ -282,7 +340,7 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     if (bits) {
       uint8_t* dst = c.pin_bits ? bits + (size_t)a * row : nullptr;
       if (!dst) {
-        if (!s.h_bits) HP_CK(cudaMallocHost(&s.h_bits, C * row));
+        if (!s.h_bits) HP_CK(cudaMallocHost(&s.h_bits, (size_t)C * row));
         dst = s.h_bits;
       }
       HP_CK(cudaMemcpyAsync(dst, s.bits_lm, (size_t)gi * row, cudaMemcpyDeviceToHost, s.st));
@@ -292,6 +350,7 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     HP_CK(cudaEventRecord(s.done, s.st));
     s.a = a;
     s.b = b;
+    a = b;
   }
   for (long long k = std::max<long long>(0, nchunks - S); k < nchunks; ++k)
     if (int rc = finish(c, h->slots[k % S])) return rc;
