@@ -21,6 +21,7 @@ outputs in HBM) used by the campaign drivers and the float64 build.
 from __future__ import annotations
 
 import dataclasses
+import threading
 
 import numpy as np
 
@@ -338,6 +339,7 @@ class HostDecoder:
                   ctypes.byref(h))
         self.handle = h.value
         self.chunk, self.slots = chunk, slots
+        self._lock = threading.Lock()      # the native decoder serves one call at a time
 
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None
@@ -352,8 +354,9 @@ class HostDecoder:
         bits = host_empty((G, n), np.uint8)
         ok = np.empty(G, dtype=bool)
         its = np.empty(G, dtype=np.int64)
-        _lib.call("qc_host_decode", self.handle, x.ctypes.data, G, float(sigma), bits.ctypes.data,
-                  post.ctypes.data, ok.ctypes.data, its.ctypes.data)
+        with self._lock:
+            _lib.call("qc_host_decode", self.handle, x.ctypes.data, G, float(sigma), bits.ctypes.data,
+                      post.ctypes.data, ok.ctypes.data, its.ctypes.data)
         return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
 
 
