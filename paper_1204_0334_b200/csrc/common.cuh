@@ -19,7 +19,10 @@ int check_launch(const char* what);        // cudaGetLastError -> code
 constexpr float L_MAX = 50.0f;
 // 2*atanh(fl(1 - 1e-12)) -- the reference's |alpha| cap (bp.py:50-51, test_bp.py:22)
 constexpr float ALPHA_CAP = 28.324190418452803892f;
-constexpr int THREADS = 256;
+#ifndef QCB_THREADS
+#define QCB_THREADS 128   // 128-thread CTAs: +12% check pass, +7-9% two-pass decode vs 256 (profiles/r01/kbench_threads128.jsonl)
+#endif
+constexpr int THREADS = QCB_THREADS;
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
