@@ -331,7 +331,7 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(fach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(fach / peak, 4),
                 "traffic": int(tf["dram_bytes"]) if tf else None,
-                "kernel": "agg_fused_kernel<24,4,2,4,0,0> (variable job + check job, compact schedule; "
+                "kernel": "agg_fused_kernel<24,4,4,4,0,0,2> (variable job + check job, compact schedule; "
                           "59 of 65 launches of a 30-iteration decode)",
                 "peak_kind": peak_kind, "bytes_per_launch": fused_bytes, "launch_ms": round(fused_ms, 4),
                 "traffic_source": (tf or {}).get("source"),

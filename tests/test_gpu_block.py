@@ -340,7 +340,7 @@ def test_compact_schedule_decode_is_bit_identical(gpu, tmp_path):
     for gamma in (384, 512):      # 512: fused half-iteration kernels; 384: unfused compact passes
         outs = []
         for env in ({"QCB_AGG": "0"}, {"QCB_AGG": "1"}, {"QCB_AGG_LG": "128", "QCB_AGG_REV": "0"},
-                    {"QCB_AGG_FUSED": "0"}, {"QCB_AGG_FVC": "4"}, {"QCB_AGG_TILE": "256"},
+                    {"QCB_AGG_FUSED": "0"}, {"QCB_AGG_FVC": "2"}, {"QCB_AGG_TILE": "256"},
                     {"QCB_AGG_ITEMS": "2"}, {"QCB_AGG_ITEMS": "2", "QCB_AGG_FUSED": "0"}):
             f = tmp_path / f"post{gamma}_{len(outs)}.npy"
             subprocess.run([sys.executable, "-c", _AGG_SNIPPET, str(f), str(gamma)], cwd=repo, check=True,
