@@ -293,7 +293,7 @@ int agg_vv() {
 }
 int agg_items() {
   static int v = env_int("QCB_AGG_ITEMS", 2);    // rows per variable thread (2: L2 prefetch of the next; +1.5%)
-  return v == 2 ? 2 : 1;
+  return v == 1 ? 1 : 2;
 }
 int agg_fused_vc() {
   static int v = env_int("QCB_AGG_FVC", 4);      // lanes per thread of the fused check job (4: +2.4% at 128-thread CTAs)
@@ -357,7 +357,7 @@ void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) 
 
 template <int DV, int VEC>
 void launch_var_v(AggArgs a, int flags, const QcGrid& g, cudaStream_t s) {
-  if (agg_items() == 2) {
+  if (agg_items() >= 2) {      // standalone variable pass: at most 2 rows per thread
     a.rows_eff = (a.rows + 1) / 2;
     launch_var_i<DV, VEC, 2>(a, flags, g, s);
   } else {
@@ -374,10 +374,14 @@ void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaSt
   }
 }
 
+#ifndef AGG_FUSED_VV
+#define AGG_FUSED_VV 4      // lanes per thread of the fused variable job (2: -12%, kbench_fused_vv_items.jsonl)
+#endif
+
 template <int DC, int DV, int VC, bool FROM_MU, int FLAGS>
 void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t s) {
-  if (agg_items() == 2) agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 2><<<grid, AGG_THREADS, 0, s>>>(f, g);
-  else agg_fused_kernel<DC, DV, VC, 4, FROM_MU, FLAGS, 1><<<grid, AGG_THREADS, 0, s>>>(f, g);
+  if (agg_items() >= 2) agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 2><<<grid, AGG_THREADS, 0, s>>>(f, g);
+  else agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 1><<<grid, AGG_THREADS, 0, s>>>(f, g);
 }
 
 template <int DC, int DV, int VC>
@@ -412,8 +416,8 @@ int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, 
                      const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s) {
   const int vc = agg_fused_vc();
   FusedArgs f;
-  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, 4, agg_reverse());
-  if (agg_items() == 2) f.v.rows_eff = (f.v.rows + 1) / 2;
+  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, agg_reverse());
+  f.v.rows_eff = (f.v.rows + agg_items() - 1) / agg_items();
   f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, vc, 0);
   f.v_bpg = blocks_per_group(f.v);
   f.c_bpg = blocks_per_group(f.c);
