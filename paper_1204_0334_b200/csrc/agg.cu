@@ -144,32 +144,73 @@ __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, i
     vload<VEC>(rec + a.gamma, sS2[j]);
     vload<VEC>(rec + 2 * a.gamma, sM[j]);
   }
+  if constexpr (VEC % 2 == 0) {
+    // lane pairs on the packed fp32 pipe: bit-identical to the scalar path below
 #pragma unroll
-  for (int j = 0; j < DV; ++j) {
+    for (int j = 0; j < DV; ++j) {
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      unsigned u = __float_as_uint(v2c[j][i]);
-      unsigned sp = __float_as_uint(sS[j][i]);
-      float f = __uint_as_float(u & 0x7fffffffu);
-      float S = __uint_as_float(sp & 0x7fffffffu);
-      float mag = (f == sM[j][i]) ? sS2[j][i] : __fsub_rn(S, f);
-      float al_ = fminf(phi_of_log2(mag), ALPHA_CAP);
-      al[j][i] = __uint_as_float(__float_as_uint(al_) | ((u ^ sp) & 0x80000000u));
+      for (int i = 0; i < VEC; i += 2) {
+        const unsigned u0 = __float_as_uint(v2c[j][i]), u1 = __float_as_uint(v2c[j][i + 1]);
+        const unsigned s0 = __float_as_uint(sS[j][i]), s1 = __float_as_uint(sS[j][i + 1]);
+        const float f0 = __uint_as_float(u0 & 0x7fffffffu), f1 = __uint_as_float(u1 & 0x7fffffffu);
+        float d0, d1;
+        get2(sub2(mk2(__uint_as_float(s0 & 0x7fffffffu), __uint_as_float(s1 & 0x7fffffffu)), mk2(f0, f1)), d0, d1);
+        const f2 mag = mk2((f0 == sM[j][i]) ? sS2[j][i] : d0, (f1 == sM[j][i + 1]) ? sS2[j][i + 1] : d1);
+        float p0, p1;
+        get2(phi_of_log2_2(mag), p0, p1);
+        al[j][i] = __uint_as_float(__float_as_uint(fminf(p0, ALPHA_CAP)) | ((u0 ^ s0) & 0x80000000u));
+        al[j][i + 1] = __uint_as_float(__float_as_uint(fminf(p1, ALPHA_CAP)) | ((u1 ^ s1) & 0x80000000u));
+      }
     }
+    // running total in increasing edge order (bp.py:179-181)
+#pragma unroll
+    for (int i = 0; i < VEC; i += 2) {
+      f2 t = mk2(tot[i], tot[i + 1]);
+#pragma unroll
+      for (int j = 0; j < DV; ++j) t = add2(t, mk2(al[j][i], al[j][i + 1]));
+      get2(t, tot[i], tot[i + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        unsigned u = __float_as_uint(v2c[j][i]);
+        unsigned sp = __float_as_uint(sS[j][i]);
+        float f = __uint_as_float(u & 0x7fffffffu);
+        float S = __uint_as_float(sp & 0x7fffffffu);
+        float mag = (f == sM[j][i]) ? sS2[j][i] : __fsub_rn(S, f);
+        float al_ = fminf(phi_of_log2(mag), ALPHA_CAP);
+        al[j][i] = __uint_as_float(__float_as_uint(al_) | ((u ^ sp) & 0x80000000u));
+      }
+    }
+    // running total in increasing edge order (bp.py:179-181)
+#pragma unroll
+    for (int j = 0; j < DV; ++j)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
   }
-  // running total in increasing edge order (bp.py:179-181)
-#pragma unroll
-  for (int j = 0; j < DV; ++j)
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
   if constexpr (!(FLAGS & AGG_LAST)) {
 #pragma unroll
     for (int j = 0; j < DV; ++j) {
       float b[VEC];
+      if constexpr (VEC % 2 == 0) {
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        float beta = clampL(__fsub_rn(tot[i], al[j][i]));
-        b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+        for (int i = 0; i < VEC; i += 2) {
+          float d0, d1;
+          get2(sub2(mk2(tot[i], tot[i + 1]), mk2(al[j][i], al[j][i + 1])), d0, d1);
+          const float be0 = clampL(d0), be1 = clampL(d1);
+          float q0, q1;
+          get2(psi_of_nat2(mk2(fabsf(be0), fabsf(be1))), q0, q1);
+          b[i] = __uint_as_float(__float_as_uint(q0) | (__float_as_uint(be0) & 0x80000000u));
+          b[i + 1] = __uint_as_float(__float_as_uint(q1) | (__float_as_uint(be1) & 0x80000000u));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          float beta = clampL(__fsub_rn(tot[i], al[j][i]));
+          b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+        }
       }
       vstore<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, b);
     }

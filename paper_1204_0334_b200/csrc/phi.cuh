@@ -90,4 +90,89 @@ __device__ __forceinline__ float phi_of_log2(float y) {
   return __fmul_rn(lg2a(__fmul_rn(__fsub_rn(2.0f, m), rcpa(m))), LN2);
 }
 
+// ---------------------------------------------------------------------------
+// Two lanes at once on the packed fp32 pipe (sm_100: FADD2 / FMUL2 / FFMA2,
+// each lane rounded exactly like the scalar instruction, so these return
+// bit-for-bit the scalar functions above; MUFU ops, compares and selects stay
+// per lane).  About 40% fewer issued instructions per phi pair.
+// ---------------------------------------------------------------------------
+struct f2 {
+  unsigned long long v;
+};
+
+__device__ __forceinline__ f2 mk2(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2 splat2(float a) { return mk2(a, a); }
+__device__ __forceinline__ void get2(f2 x, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+
+// psi_of_nat on a lane pair (x >= 0)
+__device__ __forceinline__ f2 psi_of_nat2(f2 x) {
+  const float LOG2E = 1.4426950408889634f;
+  float x0, x1;
+  get2(x, x0, x1);
+  float a0, a1;
+  get2(mul2(x, splat2(-LOG2E)), a0, a1);                       // -(x log2 e), exact sign symmetry
+  const f2 t = mk2(ex2a(a0), ex2a(a1));
+  const f2 ms = mul2(x, fma2(x, fma2(x, splat2(1.0f / 6.0f), splat2(-0.5f)), splat2(1.0f)));
+  const f2 omt = sub2(splat2(1.0f), t);
+  float ms0, ms1, o0, o1;
+  get2(ms, ms0, ms1);
+  get2(omt, o0, o1);
+  const f2 m = mk2((x0 < 0.0078125f) ? fmaxf(ms0, 1e-30f) : o0, (x1 < 0.0078125f) ? fmaxf(ms1, 1e-30f) : o1);
+  float m0, m1;
+  get2(m, m0, m1);
+  float r0, r1;
+  get2(mul2(sub2(splat2(2.0f), m), mk2(rcpa(m0), rcpa(m1))), r0, r1);
+  const float pl0 = lg2a(r0), pl1 = lg2a(r1);
+  const f2 t2 = mul2(t, t);
+  const f2 ps = mul2(t, fma2(t2, fma2(t2, splat2(0.4f * LOG2E), splat2((2.0f / 3.0f) * LOG2E)), splat2(2.0f * LOG2E)));
+  float t0, t1, ps0, ps1;
+  get2(t, t0, t1);
+  get2(ps, ps0, ps1);
+  return mk2((t0 < 0.03125f) ? ps0 : pl0, (t1 < 0.03125f) ? ps1 : pl1);
+}
+
+// phi_of_log2 on a lane pair (y >= 0)
+__device__ __forceinline__ f2 phi_of_log2_2(f2 y) {
+  const float LN2 = 0.6931471805599453f;
+  float y0, y1;
+  get2(y, y0, y1);
+  const float t0 = ex2a(-y0), t1 = ex2a(-y1);
+  const f2 ms = mul2(y, fma2(y, fma2(y, splat2(0.055504108664821580f), splat2(-0.24022650695910071f)), splat2(LN2)));
+  const f2 omt = sub2(splat2(1.0f), mk2(t0, t1));
+  float ms0, ms1, o0, o1;
+  get2(ms, ms0, ms1);
+  get2(omt, o0, o1);
+  const float m0 = (y0 < 0.011270696f) ? fmaxf(ms0, 1e-30f) : o0;
+  const float m1 = (y1 < 0.011270696f) ? fmaxf(ms1, 1e-30f) : o1;
+  float r0, r1;
+  get2(mul2(sub2(splat2(2.0f), mk2(m0, m1)), mk2(rcpa(m0), rcpa(m1))), r0, r1);
+  return mul2(mk2(lg2a(r0), lg2a(r1)), splat2(LN2));
+}
+
 }  // namespace qcb
