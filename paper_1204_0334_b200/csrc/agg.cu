@@ -108,28 +108,32 @@ __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid,
   vstore<VEC>(rec + 2 * a.gamma, oM);
 }
 
-template <int DV, int VEC, int FLAGS>
-__device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, int n, int q) {
+// check-record rows of variable n (block column l, circulant row c)
+template <int DV>
+__device__ __forceinline__ int var_rows(const QcGrid& grid, int n, int (&mrow)[DV]) {
   const int l = div_p(grid, n), c = n - l * grid.p;
-  int mrow[DV];
 #pragma unroll
   for (int j = 0; j < DV; ++j) {
     int rr = c - grid.s[j * grid.L + l];
     rr += (rr < 0) ? grid.p : 0;
     mrow[j] = j * grid.p + rr;
   }
-  float tot[VEC], v2c[DV][VEC], al[DV][VEC];
+  return l;
+}
+
+template <int DV, int VEC, int FLAGS>
+__device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid, int n, int q, int l,
+                                            const int (&mrow)[DV], float (&tot)[VEC], float (&v2c)[DV][VEC],
+                                            const float (&sS)[DV][VEC], const float (&sS2)[DV][VEC],
+                                            const float (&sM)[DV][VEC]);
+
+template <int DV, int VEC, int FLAGS>
+__device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, int n, int q) {
+  int mrow[DV];
+  const int l = var_rows<DV>(grid, n, mrow);
+  float tot[VEC], v2c[DV][VEC];
   vload<VEC>(a.mu + (size_t)n * a.gamma + q * VEC, tot);
-  if constexpr (FLAGS & AGG_FIRST) {
-    // beta^0 = mu on every edge, in the phi form the fused-init check pass saw
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      float p0 = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(tot[i]))) |
-                                 (__float_as_uint(tot[i]) & 0x80000000u));
-#pragma unroll
-      for (int j = 0; j < DV; ++j) v2c[j][i] = p0;
-    }
-  } else {
+  if constexpr (!(FLAGS & AGG_FIRST)) {
 #pragma unroll
     for (int j = 0; j < DV; ++j)
       vload<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, v2c[j]);
@@ -143,6 +147,25 @@ __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, i
     vload<VEC>(rec, sS[j]);
     vload<VEC>(rec + a.gamma, sS2[j]);
     vload<VEC>(rec + 2 * a.gamma, sM[j]);
+  }
+  var_compute<DV, VEC, FLAGS>(a, grid, n, q, l, mrow, tot, v2c, sS, sS2, sM);
+}
+
+template <int DV, int VEC, int FLAGS>
+__device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid, int n, int q, int l,
+                                            const int (&mrow)[DV], float (&tot)[VEC], float (&v2c)[DV][VEC],
+                                            const float (&sS)[DV][VEC], const float (&sS2)[DV][VEC],
+                                            const float (&sM)[DV][VEC]) {
+  float al[DV][VEC];
+  if constexpr (FLAGS & AGG_FIRST) {
+    // beta^0 = mu on every edge, in the phi form the fused-init check pass saw
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      float p0 = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(tot[i]))) |
+                                 (__float_as_uint(tot[i]) & 0x80000000u));
+#pragma unroll
+      for (int j = 0; j < DV; ++j) v2c[j][i] = p0;
+    }
   }
   if constexpr (VEC % 2 == 0) {
     // lane pairs on the packed fp32 pipe: bit-identical to the scalar path below
@@ -398,6 +421,7 @@ void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) 
 
 template <int DV, int VEC>
 void launch_var_v(AggArgs a, int flags, const QcGrid& g, cudaStream_t s) {
+
   if (agg_items() >= 2) {      // standalone variable pass: at most 2 rows per thread
     a.rows_eff = (a.rows + 1) / 2;
     launch_var_i<DV, VEC, 2>(a, flags, g, s);
