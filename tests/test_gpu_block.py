@@ -283,7 +283,7 @@ def test_compact_schedule_passes_are_bit_identical(gpu):
     import torch
     q = gpu
     from paper_1204_0334_b200 import _lib
-    for name, G in (("n18360", 256), ("code_c_like", 96)):
+    for name, G in (("n18360", 256), ("code_c_like", 96), ("code_b_like", 64)):   # float4 / float / float2 lanes
         h, exp = q.load_code(q.codes.bundled_code_path(name))
         lay = q.build_edge_layout(h)
         N, M, E = lay.n_vars, lay.n_checks, lay.edge_count
