@@ -322,8 +322,10 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
     HP_CK(cudaEventRecord(s.copied_in, s.st));
     prev_copied = s.copied_in;
-    if (prev_decoded) HP_CK(cudaStreamWaitEvent(s.st, prev_decoded, 0));
+    // the LLR conversion only needs this chunk's copy-in: it runs before the
+    // wait on the previous decode, off the serialised decode chain
     if (int rc = qc_llr_from_lane_major(N, cs, gi, s.x, sigma, s.mu, s.st)) return rc;
+    if (prev_decoded) HP_CK(cudaStreamWaitEvent(s.st, prev_decoded, 0));
     HP_CK(cudaGraphLaunch(s.graph[gsel], s.st));
     HP_CK(cudaEventRecord(s.decoded, s.st));
     prev_decoded = s.decoded;
