@@ -229,6 +229,24 @@ def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
     assert np.array_equal(r4.hard_bits, bits) and np.array_equal(r4.iterations_run, its)
 
 
+def test_graded_chunk_plans_agree(gpu, monkeypatch):
+    """The host pipeline's chunk plan (C/4, C/2, C.., remainder, C/4) and its
+    per-size graphs give the same DecodeResult for every batch size around the
+    plan's break points as one single-chunk decode."""
+    q = gpu
+    from paper_1204_0334_b200 import bp as qbp
+    lay = toy(q)
+    rng = np.random.default_rng(5)
+    y = rng.normal(1.0, 0.9, size=(700, lay.n_vars))
+    monkeypatch.setattr(qbp, "HOST_CHUNK", 1024)
+    ref = q.decode_batch(lay, y, 0.9, 9)                  # one chunk
+    monkeypatch.setattr(qbp, "HOST_CHUNK", 128)
+    for G in (129, 160, 161, 224, 300, 417, 700):
+        r = q.decode_batch(lay, y[:G], 0.9, 9)
+        for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
+            assert np.array_equal(getattr(r, f), getattr(ref, f)[:G]), (G, f)
+
+
 def test_host_pipeline_abi(gpu):
     """qc_host_* through ctypes: argument errors map to ValueError, dims round-trip."""
     import ctypes
