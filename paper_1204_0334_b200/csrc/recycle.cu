@@ -239,7 +239,7 @@ int qc_rc_ticks(const qc_plan* p, int gamma, int gamma_ref, int world, int rank,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const unsigned persist = (unsigned)nsm * 8;
+  const unsigned persist = (unsigned)nsm * (2048 / THREADS);   // 2048 threads per SM
   int rc;
   for (int t = 0; t < ticks; ++t) {
     rc_channel_kernel<<<persist, THREADS, 0, st>>>(s, c, mu, p->N);

