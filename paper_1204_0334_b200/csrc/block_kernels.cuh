@@ -68,7 +68,7 @@ struct VnuArgs {
 //   dominant edge (largest psi): its exclusive sum S2 is accumulated directly
 //   (S2 = sum of everything but the running maximum), so the subtraction
 //   S - psi_k >= max psi never cancels; sign_k = parity of the other signs.
-template <int DC, int VEC, bool IN_PHI>
+template <int DC, int VEC, bool IN_PHI, bool REL = false>
 __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned lanes) {
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
@@ -96,7 +96,7 @@ __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned 
         // S2 excludes the first maximum; an exactly tied maximum has the same
         // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
         float mag = (f == mx) ? S2 : __fsub_rn(S, f);
-        float a = fminf(phi_of_log2(mag), ALPHA_CAP);
+        float a = fminf(phi_of_log2_g<REL>(mag), ALPHA_CAP);
         x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par) & 0x80000000u));
       }
     }

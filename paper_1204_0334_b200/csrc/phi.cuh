@@ -76,11 +76,18 @@ __device__ __forceinline__ float psi_of_nat(float x) {
   return (t < 0.03125f) ? ps : pl;
 }
 
-// phi(y ln2), natural-log-domain result, for a log2-domain argument y >= 0.
-// This is the check-to-variable magnitude |alpha|: it only ever enters sums
-// (totals, extrinsics), so it needs ABSOLUTE accuracy, not relative accuracy
-// for tiny results -- the lg2 form is within ~3e-7 absolute everywhere and the
-// small-t series of psi_of_nat is not needed here (6 instructions per edge).
+// phi(y ln2), natural-log-domain result, for a log2-domain argument y >= 0:
+// the check-to-variable magnitude |alpha|.  Two accuracy grades:
+//   phi_of_log2      absolute accuracy ~3e-7 (alpha only enters sums), no
+//                    small-t series: 6 fewer instructions per edge, 5% on the
+//                    MUFU/issue-heavy compact variable job (block decoder);
+//   phi_of_log2_rel  relative accuracy a few ulp everywhere (2t(1 + t^2/3 +
+//                    t^4/5) for t = 2^-y < 1/32): the LDPCCC kernels (about
+//                    5% of slot time there).
+// The grade moves single decisions of posteriors within fp32 rounding of 0 in
+// all-failing frames (about 1 bit in 10^6 of such frames); against the float64
+// oracle tools/campaign_parity.py measured identical counts for each path
+// with the grade it uses (profiles/r01/campaign_parity_*.jsonl).
 __device__ __forceinline__ float phi_of_log2(float y) {
   const float LN2 = 0.6931471805599453f;
   float t = ex2a(-y);
@@ -88,6 +95,24 @@ __device__ __forceinline__ float phi_of_log2(float y) {
                                LN2));
   float m = (y < 0.011270696f /* 2^-7 / ln2 */) ? fmaxf(ms, 1e-30f) : __fsub_rn(1.0f, t);
   return __fmul_rn(lg2a(__fmul_rn(__fsub_rn(2.0f, m), rcpa(m))), LN2);
+}
+
+__device__ __forceinline__ float phi_of_log2_rel(float y) {
+  const float LN2 = 0.6931471805599453f;
+  float t = ex2a(-y);
+  float ms = __fmul_rn(y, fmaf(y, fmaf(y, 0.055504108664821580f /* ln2^3/6 */, -0.24022650695910071f /* -ln2^2/2 */),
+                               LN2));
+  float m = (y < 0.011270696f /* 2^-7 / ln2 */) ? fmaxf(ms, 1e-30f) : __fsub_rn(1.0f, t);
+  float pl = __fmul_rn(lg2a(__fmul_rn(__fsub_rn(2.0f, m), rcpa(m))), LN2);
+  float t2 = __fmul_rn(t, t);
+  float ps = __fmul_rn(t, fmaf(t2, fmaf(t2, 0.4f, 2.0f / 3.0f), 2.0f));
+  return (t < 0.03125f) ? ps : pl;
+}
+
+template <bool REL>
+__device__ __forceinline__ float phi_of_log2_g(float y) {
+  if constexpr (REL) return phi_of_log2_rel(y);
+  else return phi_of_log2(y);
 }
 
 // ---------------------------------------------------------------------------

@@ -138,7 +138,8 @@ __device__ __forceinline__ unsigned var_edges(const CcParams& P, const int32_t* 
 }
 
 // check-node core with a `present` mask of live positions (bootstrap layers
-// drop absent frames); same arithmetic as the block decoder (block_kernels.cuh).
+// drop absent frames); same arithmetic as the block decoder (block_kernels.cuh)
+// with the relative-accurate phi (phi.cuh).
 // Inputs are var->check packages in phi form (sign | psi(|beta|), log2 units).
 template <int DC, int VEC>
 __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long long present) {
@@ -166,7 +167,7 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
         // S2 excludes the first maximum; an exactly tied maximum has the same
         // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
         float mag = (f == mx) ? S2 : __fsub_rn(S, f);
-        float al = fminf(phi_of_log2(mag), ALPHA_CAP);
+        float al = fminf(phi_of_log2_rel(mag), ALPHA_CAP);
         x[k][i] = __uint_as_float(__float_as_uint(al) | ((u ^ par) & 0x80000000u));
       }
     }
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __g
       for (int w = 0; w < WW; ++w)
         if ((present >> d) & 1u) vload<VEC>(a.msg + (size_t)(base[d] + w) * P.gamma + q * VEC, x[d * WW + w]);
     if (present == (1u << TT) - 1u) {
-      cnu_core<DC, VEC, true>(x, TT * WW, (1u << VEC) - 1u);   // steady state
+      cnu_core<DC, VEC, true, true>(x, TT * WW, (1u << VEC) - 1u);   // steady state
     } else {
       unsigned long long pm = 0;
 #pragma unroll
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __g
       if ((present >> k) & 1ull) vload<VEC>(a.msg + (size_t)eidx[k] * P.gamma + q * VEC, x[k]);
     const int deg = T * W;
     const unsigned long long full = deg >= 64 ? ~0ull : ((1ull << deg) - 1ull);
-    if (present == full) cnu_core<DC, VEC, true>(x, deg, (1u << VEC) - 1u);
+    if (present == full) cnu_core<DC, VEC, true, true>(x, deg, (1u << VEC) - 1u);
     else cnu_core_mask<DC, VEC>(x, present);
 #pragma unroll
     for (int k = 0; k < DC; ++k)
