@@ -70,34 +70,64 @@ struct VnuArgs {
 //   S - psi_k >= max psi never cancels; sign_k = parity of the other signs.
 template <int DC, int VEC, bool IN_PHI, bool REL = false>
 __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned lanes) {
+  float S[VEC], S2[VEC], mx[VEC];
+  unsigned par[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
+    par[i] = 0;
+    S[i] = 0.0f;
+    S2[i] = 0.0f;
+    mx[i] = -1.0f;
     if (!((lanes >> i) & 1u)) continue;
-    unsigned par = 0;
-    float S = 0.0f, S2 = 0.0f, mx = -1.0f;
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
       if (k < deg) {
         float b = x[k][i];
         unsigned sb = __float_as_uint(b) & 0x80000000u;
         float f = IN_PHI ? fabsf(b) : psi_of_nat(fabsf(b));
-        par ^= sb;
-        S2 = (f > mx) ? S : __fadd_rn(S2, f);
-        mx = fmaxf(mx, f);
-        S = __fadd_rn(S, f);
+        par[i] ^= sb;
+        S2[i] = (f > mx[i]) ? S[i] : __fadd_rn(S2[i], f);
+        mx[i] = fmaxf(mx[i], f);
+        S[i] = __fadd_rn(S[i], f);
         if (!IN_PHI) x[k][i] = __uint_as_float(__float_as_uint(f) | sb);
       }
     }
+  }
+  // S2 excludes the first maximum; an exactly tied maximum has the same
+  // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
+  if constexpr (VEC % 2 == 0) {
+    // lane pairs on the packed fp32 pipe (bit-identical to the scalar form)
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
       if (k < deg) {
-        unsigned u = __float_as_uint(x[k][i]);
-        float f = __uint_as_float(u & 0x7fffffffu);
-        // S2 excludes the first maximum; an exactly tied maximum has the same
-        // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
-        float mag = (f == mx) ? S2 : __fsub_rn(S, f);
-        float a = fminf(phi_of_log2_g<REL>(mag), ALPHA_CAP);
-        x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par) & 0x80000000u));
+#pragma unroll
+        for (int i = 0; i < VEC; i += 2) {
+          const unsigned u0 = __float_as_uint(x[k][i]), u1 = __float_as_uint(x[k][i + 1]);
+          const float f0 = __uint_as_float(u0 & 0x7fffffffu), f1 = __uint_as_float(u1 & 0x7fffffffu);
+          float d0, d1;
+          get2(sub2(mk2(S[i], S[i + 1]), mk2(f0, f1)), d0, d1);
+          float p0, p1;
+          get2(phi_of_log2_g2<REL>(mk2((f0 == mx[i]) ? S2[i] : d0, (f1 == mx[i + 1]) ? S2[i + 1] : d1)), p0, p1);
+          if ((lanes >> i) & 1u)
+            x[k][i] = __uint_as_float(__float_as_uint(fminf(p0, ALPHA_CAP)) | ((u0 ^ par[i]) & 0x80000000u));
+          if ((lanes >> (i + 1)) & 1u)
+            x[k][i + 1] = __uint_as_float(__float_as_uint(fminf(p1, ALPHA_CAP)) | ((u1 ^ par[i + 1]) & 0x80000000u));
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      if (!((lanes >> i) & 1u)) continue;
+#pragma unroll
+      for (int k = 0; k < DC; ++k) {
+        if (k < deg) {
+          unsigned u = __float_as_uint(x[k][i]);
+          float f = __uint_as_float(u & 0x7fffffffu);
+          float mag = (f == mx[i]) ? S2[i] : __fsub_rn(S[i], f);
+          float a = fminf(phi_of_log2_g<REL>(mag), ALPHA_CAP);
+          x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par[i]) & 0x80000000u));
+        }
       }
     }
   }

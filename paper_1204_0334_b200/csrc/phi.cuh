@@ -200,4 +200,35 @@ __device__ __forceinline__ f2 phi_of_log2_2(f2 y) {
   return mul2(mk2(lg2a(r0), lg2a(r1)), splat2(LN2));
 }
 
+// phi_of_log2_rel on a lane pair (y >= 0)
+__device__ __forceinline__ f2 phi_of_log2_rel_2(f2 y) {
+  const float LN2 = 0.6931471805599453f;
+  float y0, y1;
+  get2(y, y0, y1);
+  const f2 t = mk2(ex2a(-y0), ex2a(-y1));
+  const f2 ms = mul2(y, fma2(y, fma2(y, splat2(0.055504108664821580f), splat2(-0.24022650695910071f)), splat2(LN2)));
+  const f2 omt = sub2(splat2(1.0f), t);
+  float ms0, ms1, o0, o1;
+  get2(ms, ms0, ms1);
+  get2(omt, o0, o1);
+  const float m0 = (y0 < 0.011270696f) ? fmaxf(ms0, 1e-30f) : o0;
+  const float m1 = (y1 < 0.011270696f) ? fmaxf(ms1, 1e-30f) : o1;
+  float r0, r1;
+  get2(mul2(sub2(splat2(2.0f), mk2(m0, m1)), mk2(rcpa(m0), rcpa(m1))), r0, r1);
+  float pl0, pl1;
+  get2(mul2(mk2(lg2a(r0), lg2a(r1)), splat2(LN2)), pl0, pl1);
+  const f2 t2 = mul2(t, t);
+  const f2 ps = mul2(t, fma2(t2, fma2(t2, splat2(0.4f), splat2(2.0f / 3.0f)), splat2(2.0f)));
+  float t0, t1, ps0, ps1;
+  get2(t, t0, t1);
+  get2(ps, ps0, ps1);
+  return mk2((t0 < 0.03125f) ? ps0 : pl0, (t1 < 0.03125f) ? ps1 : pl1);
+}
+
+template <bool REL>
+__device__ __forceinline__ f2 phi_of_log2_g2(f2 y) {
+  if constexpr (REL) return phi_of_log2_rel_2(y);
+  else return phi_of_log2_2(y);
+}
+
 }  // namespace qcb
