@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -336,10 +337,24 @@ __global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __gri
     for (int k = 0; k < DV; ++k)
       if ((present >> k) & 1u) {
         float b[VEC];
+        if constexpr (VEC % 2 == 0) {
+          // lane pairs on the packed fp32 pipe (bit-identical to the scalar form)
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-          float beta = clampL(__fsub_rn(tot[i], am[k][i]));   // stored in phi form
-          b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+          for (int i = 0; i < VEC; i += 2) {
+            float d0, d1;
+            get2(sub2(mk2(tot[i], tot[i + 1]), mk2(am[k][i], am[k][i + 1])), d0, d1);
+            const float be0 = clampL(d0), be1 = clampL(d1);   // stored in phi form
+            float q0, q1;
+            get2(psi_of_nat2(mk2(fabsf(be0), fabsf(be1))), q0, q1);
+            b[i] = __uint_as_float(__float_as_uint(q0) | (__float_as_uint(be0) & 0x80000000u));
+            b[i + 1] = __uint_as_float(__float_as_uint(q1) | (__float_as_uint(be1) & 0x80000000u));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) {
+            float beta = clampL(__fsub_rn(tot[i], am[k][i]));   // stored in phi form
+            b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+          }
         }
         vstore<VEC>(a.msg + (size_t)e[k] * P.gamma + q * VEC, b);
       }
