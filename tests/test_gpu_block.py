@@ -160,6 +160,29 @@ def test_irregular_code_against_oracle(gpu):
     assert not r.hard_bits.any() and r.syndrome_ok.all()
 
 
+@pytest.mark.parametrize("J,L,p,G", [(3, 6, 31, 128), (3, 12, 29, 96), (2, 8, 37, 64), (4, 16, 23, 256)])
+def test_compact_schedule_shapes_against_oracle(gpu, J, L, p, G):
+    """Every (d_v, d_c) instantiation of the compact schedule (d_v 2-4, d_c 6-16,
+    float / float2 / float4 lanes) decodes a regular QC code like the float64
+    oracle: decisions, syndromes and iteration counts bit-exact after 15
+    iterations, posteriors within 1e-4 after 3.  (Posterior deviations grow
+    with iterations on the (3, 6) array code -- 2.7e-4 after 15, for either phi
+    grade -- its short cycles amplify fp32 rounding; the decisions still agree,
+    tools/posterior_error_diag.py.)"""
+    q = gpu
+    exp = q.multiplicative_shifts(J, L, p)
+    lay = q.build_edge_layout(q.expand_qc(exp))
+    olay = oqc.qc_layout(exp.shifts, p)
+    rng = np.random.default_rng(J * 100 + L)
+    y = rng.normal(1.0, 0.75, size=(G, lay.n_vars))
+    r = q.decode_batch(lay, y, 0.75, 15)
+    bits, post, ok, its = obp.decode_llr(olay, obp.channel_llrs(y, 0.75), 15)
+    assert np.array_equal(r.hard_bits, bits) and np.array_equal(r.syndrome_ok, ok)
+    assert np.array_equal(r.iterations_run, its)
+    r3 = q.decode_batch(lay, y, 0.75, 3)
+    close(r3.posteriors, obp.decode_llr(olay, obp.channel_llrs(y, 0.75), 3)[1])
+
+
 def test_early_stop_semantics(gpu):
     q = gpu
     lay = toy(q)
