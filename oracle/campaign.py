@@ -55,7 +55,12 @@ def stream_task(s: int):
     return fr, be, fe
 
 
-def _run(task, init_kw, stop, max_frames, workers):
+def ping(_):
+    """No-op task: brings a pool's workers up outside a timed region."""
+    return 0
+
+
+def _run(task, init_kw, stop, max_frames, workers, start_method="fork"):
     fr = be = fe = 0
     if workers <= 1:
         _init(**init_kw)
@@ -65,7 +70,9 @@ def _run(task, init_kw, stop, max_frames, workers):
             f, e1, e2 = task(b)
             fr += f; be += e1; fe += e2
     else:
-        with multiprocessing.get_context("fork").Pool(
+        # "spawn" from processes that initialised CUDA or thread pools (a forked
+        # child of such a process can abort in its after-fork hooks)
+        with multiprocessing.get_context(start_method).Pool(
                 workers, initializer=_set_ctx, initargs=(init_kw,)) as pool:
             for f, e1, e2 in pool.imap(task, itertools.count()):
                 fr += f; be += e1; fe += e2
@@ -80,22 +87,22 @@ def _set_ctx(kw):
 
 
 def block_point(lay, ebn0_db, point_index=0, *, iters=30, gamma=32, seed=0,
-                stop=100, max_frames=1_000_000, workers=1, early_stop=False):
+                stop=100, max_frames=1_000_000, workers=1, early_stop=False, start_method="fork"):
     rate = 1.0 - lay.n_checks / lay.n_vars
     sigma = channel.ebn0_to_sigma(ebn0_db, rate)
     kw = dict(lay=lay, seed=seed, sigma=sigma, gamma=gamma, iters=iters,
               lane0=point_index << 32, early=early_stop)
-    return _run(block_task, kw, stop, max_frames, workers)
+    return _run(block_task, kw, stop, max_frames, workers, start_method)
 
 
 def stream_point(code, ebn0_db, point_index=0, *, processors=20, gamma=32, seed=0,
-                 stop=100, max_frames=1_000_000, workers=1, segment_frames=None):
+                 stop=100, max_frames=1_000_000, workers=1, segment_frames=None, start_method="fork"):
     window = processors * (code.ms + 1)
     counted = segment_frames or max(2 * (window - 1), 64)
     sigma = channel.ebn0_to_sigma(ebn0_db, (code.c - code.cb) / code.c)
     kw = dict(code=code, seed=seed, sigma=sigma, gamma=gamma, I=processors,
               pushes=counted + window - 1, lane0=point_index << 32)
-    return _run(stream_task, kw, stop, max_frames, workers)
+    return _run(stream_task, kw, stop, max_frames, workers, start_method)
 
 
 def sum_counts(rows):

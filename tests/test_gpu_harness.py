@@ -138,15 +138,15 @@ def test_n18360_failing_frames_match_oracle_f64(gpu):
     decoder never converges there); on n18360 at 2.9 dB (FER ~0.7) the GPU
     campaign's frame / bit / frame-error counts equal the float64 oracle's
     (profiles/r01/campaign_parity_n18360.jsonl: also 2048 frames at 2.8/3.0/3.2 dB)."""
-    import os
     q = gpu
     from oracle import campaign, qc
     h, exp = q.load_code(q.codes.bundled_code_path("n18360"))
     lay = q.build_edge_layout(h)
     cfg = q.SimulationConfig("n18360", [2.9], iterations=30, gamma=32, stop_block_errors=2**62,
-                             max_frames=256, seed=0)
+                             max_frames=128, seed=0)
     g = q.run_block_simulation(lay, cfg)[0]
+    # serial oracle: never fork a process that has initialised CUDA / thread pools
     o = campaign.block_point(qc.qc_layout(exp.shifts, exp.p), 2.9, 0, iters=30, gamma=32, seed=0,
-                             stop=2**62, max_frames=256, workers=min(8, len(os.sched_getaffinity(0))))
+                             stop=2**62, max_frames=128, workers=1)
     assert (g.frames, g.bit_errors, g.frame_errors) == tuple(o)
-    assert g.frame_errors > 64
+    assert g.frame_errors > 32

@@ -38,7 +38,7 @@ def main():
             g = q.run_stream_simulation(code, cfg)[0]
             t0 = time.time()
             o = campaign.stream_point(ocode, db, 0, processors=args.stream, gamma=32, seed=0, stop=2**62,
-                                      max_frames=args.frames, workers=workers)
+                                      max_frames=args.frames, workers=workers, start_method="spawn")
             print(json.dumps({"code": args.code + "'", "I": args.stream, "ebn0_db": db,
                               "gpu": [g.frames, g.bit_errors, g.frame_errors], "oracle_f64": list(o),
                               "identical": [g.frames, g.bit_errors, g.frame_errors] == list(o),
@@ -50,7 +50,7 @@ def main():
         g = q.run_block_simulation(lay, cfg)[0]
         t0 = time.time()
         o = campaign.block_point(olay, db, 0, iters=args.iters, gamma=32, seed=0, stop=2**62,
-                                 max_frames=args.frames, workers=workers)
+                                 max_frames=args.frames, workers=workers, start_method="spawn")
         print(json.dumps({"code": args.code, "ebn0_db": db, "gpu": [g.frames, g.bit_errors, g.frame_errors],
                           "oracle_f64": list(o), "identical": [g.frames, g.bit_errors, g.frame_errors] == list(o),
                           "oracle_s": round(time.time() - t0, 1)}), flush=True)

@@ -85,7 +85,7 @@ def main():
     if args.cpu:
         cores = len(os.sched_getaffinity(0))
         for I in args.cpu_I:
-            with mp.get_context("fork").Pool(cores) as pool:
+            with mp.get_context("spawn").Pool(cores) as pool:   # this process initialised CUDA
                 ts = pool.map(_cpu_slot_time, [(args.code, I, 32, k) for k in range(cores)])
             t = sorted(ts)[len(ts) // 2]
             window = I * (code.ms + 1)
