@@ -383,13 +383,15 @@ def host_array(a: np.ndarray) -> np.ndarray:
 def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool,
                   pinned_input: bool = False) -> HostDecoder:
     import torch
-    chunk = min(HOST_CHUNK, pad32(gamma))
+    # small batches: chunk rounded up to a multiple of 64 lanes (<= 8 distinct
+    # decoders below HOST_CHUNK; each holds device buffers and captured graphs)
+    chunk = min(HOST_CHUNK, pad32(gamma) if gamma <= 32 else (gamma + 63) // 64 * 64)
     slots = (HOST_SLOTS_PINNED if pinned_input else HOST_SLOTS) if gamma > chunk else 1
     cache = layout.__dict__.setdefault("_host_decoders", {})
     key = (chunk, slots, iterations, bool(early_stop), torch.cuda.current_device())
     dec = cache.get(key)
     if dec is None:
-        if len(cache) >= 6:
+        if len(cache) >= 12:
             cache.clear()
         dec = HostDecoder(layout, chunk, slots, iterations, early_stop)
         cache[key] = dec
