@@ -1,0 +1,40 @@
+#!/usr/bin/env python
+"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
+synccheck): channel, fused compact decode, two-pass early-stop decode, host
+pipeline with ragged chunks, LDPCCC slots, recycling campaign.
+
+  compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import numpy as np
+    import paper_1204_0334_b200 as q
+    from paper_1204_0334_b200 import bp as qbp
+    qbp.HOST_CHUNK = 256
+    exp = q.multiplicative_shifts(4, 24, 31)            # (4, 24) grid: fused compact kernels
+    lay = q.build_edge_layout(q.expand_qc(exp))
+    cfg = q.ChannelConfig(2.5, 5 / 6, seed=3, gamma=600)
+    y = q.simulate_block(cfg, lay.n_vars)                 # on-device channel
+    r = q.decode_batch(lay, y, cfg.sigma, 6)              # host pipeline, 256-lane chunks, ragged tail
+    r2 = q.decode_batch(lay, y[:100], cfg.sigma, 6, early_stop=True)
+    assert r.hard_bits.shape == y.shape and r2.iterations_run.max() <= 6
+    toy = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    q.decode_batch(toy, np.random.default_rng(1).normal(1, 0.8, (70, toy.n_vars)), 0.8, 5)
+    code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 11))
+    dec = q.StreamDecoder(code, 2, gamma=3)
+    for t in range(12):
+        dec.push_frame(np.random.default_rng(t).normal(1, 0.8, (3, code.c)), 0.8)
+    dec.flush()
+    sim = q.SimulationConfig("t", [2.8], iterations=8, gamma=32, stop_block_errors=10**9, max_frames=256,
+                             seed=1, early_stop=True)
+    q.run_block_simulation(lay, sim, gamma_kernel=128, recycle=True)
+    print("sanitize smoke ok")
+
+
+if __name__ == "__main__":
+    main()
