@@ -23,6 +23,7 @@
 // check records a variable pass gathers (24 reads per record) stay L2
 // resident: LG = 512 lanes -> 3060 x 512 x 12 B = 18.8 MB for n18360.
 #include <cstdlib>
+#include <utility>
 
 #include "block_kernels.cuh"
 
@@ -53,6 +54,13 @@ struct AggArgs {
 #endif
 
 enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
+
+// Programmatic dependent launch (sm_90+): each compact-schedule kernel lets the
+// next one in the stream be scheduled immediately and waits for its
+// predecessor's results only right before its first dependent load, so the
+// launch latency and index math of kernel k+1 overlap the tail of kernel k.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // block (bx within its lane group, group index) + thread -> (row, lane vector q).
 // Lane-group major: every row of one group of lanes before the next group.
@@ -284,14 +292,20 @@ __device__ __forceinline__ void var_items(const AggArgs& a, const QcGrid& grid, 
 // grid = (blocks per lane group, groups)
 template <int DC, int VEC, bool FROM_MU>
 __global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
   int m, q;
-  if (agg_map(a, blockIdx.x, blockIdx.y, m, q)) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
+  const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q);
+  pdl_wait();
+  if (on) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
 }
 
 template <int DV, int VEC, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
   int n, q;
-  if (agg_map(a, blockIdx.x, blockIdx.y, n, q)) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
+  const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q);
+  pdl_wait();
+  if (on) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
 }
 
 // One launch, two independent jobs on disjoint lane windows: the variable pass
@@ -312,6 +326,8 @@ __device__ __forceinline__ unsigned div_magic(unsigned x, unsigned long long m) 
 
 template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
+  pdl_wait();
   int row, q;
   if (blockIdx.x == f.R) {
     const unsigned b = blockIdx.y, g = div_magic(b, f.c_magic);
@@ -325,6 +341,29 @@ __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(Fu
 }
 
 namespace {
+
+int env_int(const char* name, int dflt);
+
+int agg_pdl() {
+  static int v = env_int("QCB_AGG_PDL", 1);
+  return v;
+}
+
+// launch with the programmatic-stream-serialization attribute (PDL)
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(AGG_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = agg_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -395,8 +434,8 @@ AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_
 template <int DC, int VEC>
 void launch_check_v(const AggArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
-  if (from_mu) agg_check_kernel<DC, VEC, true><<<nb, AGG_THREADS, 0, s>>>(a, g);
-  else agg_check_kernel<DC, VEC, false><<<nb, AGG_THREADS, 0, s>>>(a, g);
+  if (from_mu) launch_k(agg_check_kernel<DC, VEC, true>, nb, s, a, g);
+  else launch_k(agg_check_kernel<DC, VEC, false>, nb, s, a, g);
 }
 
 template <int DC>
@@ -412,10 +451,10 @@ template <int DV, int VEC, int ITEMS>
 void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
   switch (flags) {
-    case 0: agg_var_kernel<DV, VEC, 0, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g); break;
-    case AGG_FIRST: agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g); break;
-    case AGG_LAST: agg_var_kernel<DV, VEC, AGG_LAST, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g); break;
-    default: agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS><<<nb, AGG_THREADS, 0, s>>>(a, g);
+    case 0: launch_k(agg_var_kernel<DV, VEC, 0, ITEMS>, nb, s, a, g); break;
+    case AGG_FIRST: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS>, nb, s, a, g); break;
+    case AGG_LAST: launch_k(agg_var_kernel<DV, VEC, AGG_LAST, ITEMS>, nb, s, a, g); break;
+    default: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS>, nb, s, a, g);
   }
 }
 
@@ -445,8 +484,8 @@ void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaSt
 
 template <int DC, int DV, int VC, bool FROM_MU, int FLAGS>
 void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t s) {
-  if (agg_items() >= 2) agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 2><<<grid, AGG_THREADS, 0, s>>>(f, g);
-  else agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 1><<<grid, AGG_THREADS, 0, s>>>(f, g);
+  if (agg_items() >= 2) launch_k(agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 2>, grid, s, f, g);
+  else launch_k(agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 1>, grid, s, f, g);
 }
 
 template <int DC, int DV, int VC>
