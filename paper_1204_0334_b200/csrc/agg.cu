@@ -59,9 +59,6 @@ enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
 // next one in the stream be scheduled immediately and waits for its
 // predecessor's results only right before its first dependent load, so the
 // launch latency and index math of kernel k+1 overlap the tail of kernel k.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // block (bx within its lane group, group index) + thread -> (row, lane vector q).
 // Lane-group major: every row of one group of lanes before the next group.
 __device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned grp, int& row, int& q) {
@@ -344,25 +341,9 @@ namespace {
 
 int env_int(const char* name, int dflt);
 
-int agg_pdl() {
-  static int v = env_int("QCB_AGG_PDL", 1);
-  return v;
-}
-
-// launch with the programmatic-stream-serialization attribute (PDL)
 template <typename... KArgs, typename... Args>
-void launch_k(void (*kern)(KArgs...), dim3 grid, cudaStream_t s, Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(AGG_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = agg_pdl() ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+void launch_k(void (*kern)(KArgs...), dim3 grid, cudaStream_t s, Args... args) {
+  launch_pdl(kern, grid, AGG_THREADS, s, args...);
 }
 
 int env_int(const char* name, int dflt) {

@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(THREADS) channel_kernel(ChanArgs a) {
   __shared__ double qu[THREADS / 32][128];        // central from the front, tail from the back
   __shared__ unsigned char qslot[THREADS / 32][128];
   __shared__ double res[THREADS / 32][128];       // slot k*32 + lane
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (a.t_dev) a.start += (uint64_t)((*a.t_dev + a.t_add) * a.t_mul);
@@ -111,7 +113,7 @@ int launch_channel(uint64_t k0, uint64_t k1, uint64_t lane0, uint64_t start, int
   long long nblk = (long long)(((start & 3) + (uint64_t)n + 3) >> 2);
   long long threads = nblk * gamma;
   if (threads == 0) return 0;
-  channel_kernel<<<blocks_for(threads), THREADS, 0, s>>>(a);
+  launch_pdl(channel_kernel, dim3(blocks_for(threads)), THREADS, s, a);
   return check_launch("channel");
 }
 // device-indexed variant for graph-captured slots: positions start at
@@ -128,7 +130,7 @@ int launch_channel_t(uint64_t k0, uint64_t k1, uint64_t lane0, const uint64_t* l
   // the start may be known only on the device: cover the worst-case block count
   long long threads = (long long)((n + 3) / 4 + 1) * gamma;
   if (threads == 0) return 0;
-  channel_kernel<<<blocks_for(threads), THREADS, 0, s>>>(a);
+  launch_pdl(channel_kernel, dim3(blocks_for(threads)), THREADS, s, a);
   return check_launch("channel");
 }
 }  // namespace qcb

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -19,6 +20,13 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail_arg(const std::string& msg) { set_error(msg); return -1; }
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("QCB_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
 int fail_rt(const std::string& msg) { set_error(msg); return 1; }
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();

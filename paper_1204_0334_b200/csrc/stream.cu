@@ -179,6 +179,8 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
 // Also folds the previous slot's emitted-frame bit count into the lane counters.
 template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
 __global__ void __launch_bounds__(CC_THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+  pdl_trigger();
+  pdl_wait();
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC, window = P.I * T;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -216,6 +218,8 @@ __global__ void __launch_bounds__(CC_THREADS) entry_kernel(SlotArgs a, const __g
 // common shapes) so the edge walk fully unrolls; 0 = runtime values.
 template <int DC, int VEC, bool QC, int TT = 0, int WW = 0>
 __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+  pdl_trigger();
+  pdl_wait();
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -308,6 +312,8 @@ __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __g
 // ---- variable phase: processors i = 1..I refresh frame j = t - iT + 1 ------
 template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
 __global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+  pdl_trigger();
+  pdl_wait();
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -408,24 +414,24 @@ void launch_entry(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
   long long n = (long long)P.c * (P.gamma / vec);
   unsigned nb = blocks_for(std::max<long long>(n, P.gamma), CC_THREADS);
-  if (vec == 4) entry_kernel<DV, 4, QC, TT, SJ><<<nb, CC_THREADS, 0, s>>>(a, P);
-  else if (vec == 2) entry_kernel<DV, 2, QC, TT, SJ><<<nb, CC_THREADS, 0, s>>>(a, P);
-  else entry_kernel<DV, 1, QC, TT, SJ><<<nb, CC_THREADS, 0, s>>>(a, P);
+  if (vec == 4) launch_pdl(entry_kernel<DV, 4, QC, TT, SJ>, dim3(nb), CC_THREADS, s, a, P);
+  else if (vec == 2) launch_pdl(entry_kernel<DV, 2, QC, TT, SJ>, dim3(nb), CC_THREADS, s, a, P);
+  else launch_pdl(entry_kernel<DV, 1, QC, TT, SJ>, dim3(nb), CC_THREADS, s, a, P);
 }
 template <int DC, bool QC, int TT = 0, int WW = 0>
 void launch_check(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, DC > 24 ? 1 : 2);
   long long n = (long long)P.I * P.cb * (P.gamma / vec);
-  if (vec == 2) check_kernel<DC, 2, QC, TT, WW><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
-  else check_kernel<DC, 1, QC, TT, WW><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
+  if (vec == 2) launch_pdl(check_kernel<DC, 2, QC, TT, WW>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
+  else launch_pdl(check_kernel<DC, 1, QC, TT, WW>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
 }
 template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_var(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
   long long n = (long long)P.I * P.c * (P.gamma / vec);
-  if (vec == 4) var_kernel<DV, 4, QC, TT, SJ><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
-  else if (vec == 2) var_kernel<DV, 2, QC, TT, SJ><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
-  else var_kernel<DV, 1, QC, TT, SJ><<<blocks_for(n, CC_THREADS), CC_THREADS, 0, s>>>(a, P);
+  if (vec == 4) launch_pdl(var_kernel<DV, 4, QC, TT, SJ>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
+  else if (vec == 2) launch_pdl(var_kernel<DV, 2, QC, TT, SJ>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
+  else launch_pdl(var_kernel<DV, 1, QC, TT, SJ>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
 }
 
 template <int DV, bool QC>
