@@ -41,6 +41,8 @@ struct AggArgs {
   int groups;          // lane groups in the window
   int reverse;         // visit lane groups last-to-first
   int rows_eff;        // rows the grid covers (rows / items per thread, rounded up)
+  const uint32_t* active;   // early stop: lane mask words (gamma / 32) or null
+  const int32_t* done;      // early stop: this window's "all lanes frozen" flag or null
 };
 
 // min CTAs/SM for the variable job: 4 x 256 threads caps it at 64 registers,
@@ -53,7 +55,9 @@ struct AggArgs {
 #define AGG_VAR_MINB (1024 / AGG_THREADS)
 #endif
 
-enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG };
+// AGG_ES: early stop (bp.py:242-256): frozen lanes keep their packages and
+// posteriors; post and hard bits are written every iteration for live lanes
+enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG, AGG_ES = 4 };
 
 // Programmatic dependent launch (sm_90+): each compact-schedule kernel lets the
 // next one in the stream be scheduled immediately and waits for its
@@ -72,6 +76,7 @@ __device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned 
 
 template <int DC, int VEC, bool FROM_MU>
 __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid, int m, int q) {
+  if (a.active && lane_bits_of(a.active, q * VEC, VEC) == 0) return;   // frozen lanes keep stale records
   int jrow = 0, r = 0;
   if constexpr (FROM_MU) {
     jrow = div_p(grid, m);
@@ -134,6 +139,12 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
 
 template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, int n, int q) {
+  if constexpr ((FLAGS & AGG_ES) != 0) {
+    if (lane_bits_of(a.active, q * VEC, VEC) == 0) {   // every lane of the vector frozen
+      if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, 0u, true);
+      return;
+    }
+  }
   int mrow[DV];
   const int l = var_rows<DV>(grid, n, mrow);
   float tot[VEC], v2c[DV][VEC];
@@ -218,6 +229,8 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
 #pragma unroll
       for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
   }
+  unsigned lanes = (1u << VEC) - 1u;
+  if constexpr ((FLAGS & AGG_ES) != 0) lanes = lane_bits_of(a.active, q * VEC, VEC);
   if constexpr (!(FLAGS & AGG_LAST)) {
 #pragma unroll
     for (int j = 0; j < DV; ++j) {
@@ -240,9 +253,14 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
           b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
         }
       }
+      if constexpr ((FLAGS & AGG_ES) != 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) b[i] = ((lanes >> i) & 1u) ? b[i] : v2c[j][i];   // frozen: unchanged
+      }
       vstore<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, b);
     }
-  } else {
+  }
+  if constexpr ((FLAGS & (AGG_LAST | AGG_ES)) != 0) {
     float pst[VEC];
     unsigned bits = 0;
 #pragma unroll
@@ -250,7 +268,16 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
       pst[i] = clampL(tot[i]);
       bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
     }
-    if (a.post) vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
+    bits &= lanes;
+    if (a.post) {
+      if (lanes == (1u << VEC) - 1u) {
+        vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
+      } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+          if ((lanes >> i) & 1u) a.post[(size_t)n * a.gamma + q * VEC + i] = pst[i];
+      }
+    }
     // whole warps share one row (gw >= 32), so the shuffle is safe
     if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, true);
   }
@@ -293,6 +320,7 @@ __global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const
   int m, q;
   const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q);
   pdl_wait();
+  if (a.done && *a.done) return;
   if (on) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
 }
 
@@ -302,6 +330,7 @@ __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggA
   int n, q;
   const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q);
   pdl_wait();
+  if (a.done && *a.done) return;
   if (on) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
 }
 
@@ -327,9 +356,11 @@ __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(Fu
   pdl_wait();
   int row, q;
   if (blockIdx.x == f.R) {
+    if (f.c.done && *f.c.done) return;
     const unsigned b = blockIdx.y, g = div_magic(b, f.c_magic);
     if (agg_map(f.c, b - g * f.c_bpg, g, row, q)) check_body<DC, VC, FROM_MU>(f.c, grid, row, q);
   } else {
+    if (f.v.done && *f.v.done) return;
     const unsigned b = blockIdx.y * f.R + blockIdx.x;
     if (b >= f.nbv) return;
     const unsigned g = div_magic(b, f.v_magic);
@@ -407,7 +438,8 @@ dim3 agg_grid(const AggArgs& a, int) { return dim3(blocks_per_group(a), (unsigne
 // pass arguments over the lane window [lane0, lane0 + lanes) of a gamma-wide store
 AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_t* hb, int rows, int gamma,
                   int lane0, int lanes, int vec, int reverse) {
-  AggArgs a{msgs, mu, agg, post, hb, rows, gamma, lane0 / vec, pick_lg_gw(lanes, vec), 0, reverse, rows};
+  AggArgs a{msgs, mu, agg, post, hb, rows, gamma, lane0 / vec, pick_lg_gw(lanes, vec), 0, reverse, rows,
+            nullptr, nullptr};
   a.groups = (lanes / vec) >> a.lg_gw;
   return a;
 }
@@ -435,6 +467,10 @@ void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) 
     case 0: launch_k(agg_var_kernel<DV, VEC, 0, ITEMS>, nb, s, a, g); break;
     case AGG_FIRST: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS>, nb, s, a, g); break;
     case AGG_LAST: launch_k(agg_var_kernel<DV, VEC, AGG_LAST, ITEMS>, nb, s, a, g); break;
+    case AGG_ES | AGG_LAST: launch_k(agg_var_kernel<DV, VEC, AGG_ES | AGG_LAST, ITEMS>, nb, s, a, g); break;
+    case AGG_ES | AGG_FIRST | AGG_LAST:
+      launch_k(agg_var_kernel<DV, VEC, AGG_ES | AGG_FIRST | AGG_LAST, ITEMS>, nb, s, a, g);
+      break;
     default: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS>, nb, s, a, g);
   }
 }
@@ -476,6 +512,12 @@ int launch_fused_v(const FusedArgs& f, dim3 grid, bool from_mu, int flags, const
   else if (!from_mu && flags == AGG_FIRST) launch_fused_t<DC, DV, VC, false, AGG_FIRST>(f, grid, g, s);
   else if (!from_mu && flags == 0) launch_fused_t<DC, DV, VC, false, 0>(f, grid, g, s);
   else if (!from_mu && flags == AGG_LAST) launch_fused_t<DC, DV, VC, false, AGG_LAST>(f, grid, g, s);
+  else if (from_mu && flags == (AGG_ES | AGG_FIRST)) launch_fused_t<DC, DV, VC, true, AGG_ES | AGG_FIRST>(f, grid, g, s);
+  else if (from_mu && flags == (AGG_ES | AGG_FIRST | AGG_LAST))
+    launch_fused_t<DC, DV, VC, true, AGG_ES | AGG_FIRST | AGG_LAST>(f, grid, g, s);
+  else if (!from_mu && flags == (AGG_ES | AGG_FIRST)) launch_fused_t<DC, DV, VC, false, AGG_ES | AGG_FIRST>(f, grid, g, s);
+  else if (!from_mu && flags == AGG_ES) launch_fused_t<DC, DV, VC, false, AGG_ES>(f, grid, g, s);
+  else if (!from_mu && flags == (AGG_ES | AGG_LAST)) launch_fused_t<DC, DV, VC, false, AGG_ES | AGG_LAST>(f, grid, g, s);
   else return fail_arg("fused compact pass: unsupported (from_mu, flags) combination");
   return 0;
 }
@@ -496,14 +538,28 @@ bool agg_fused_eligible(const qc_plan* p, int gamma) {
          ((p->L == 24 && p->J == 4) || (p->L == 4 && p->J == 2));
 }
 
+int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
+                        float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
+                        const uint32_t* active, const int32_t* v_done, const int32_t* c_done, cudaStream_t s);
+
 // variable pass on lanes [v0, v0 + lanes) fused with the check pass on lanes [c0, c0 + lanes)
 int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
                      const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s) {
+  return launch_agg_fused_es(p, gamma, lanes, v0, flags, c0, from_mu, msgs, mu, agg, post, hb, nullptr, nullptr,
+                             nullptr, s);
+}
+
+int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
+                        float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
+                        const uint32_t* active, const int32_t* v_done, const int32_t* c_done, cudaStream_t s) {
   const int vc = agg_fused_vc();
   FusedArgs f;
   f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, agg_reverse());
   f.v.rows_eff = (f.v.rows + agg_items() - 1) / agg_items();
   f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, vc, 0);
+  f.v.active = f.c.active = active;
+  f.v.done = v_done;
+  f.c.done = c_done;
   f.v_bpg = blocks_per_group(f.v);
   f.c_bpg = blocks_per_group(f.c);
   f.v_magic = magic40(f.v_bpg);
@@ -519,11 +575,13 @@ int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, 
   return check_launch("agg_fused");
 }
 
-// single passes over a lane window
+// single passes over a lane window (active / done: early-stop mask and flag)
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s);
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active = nullptr,
+                       const int32_t* done = nullptr);
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
-                     const float* agg, float* post, uint32_t* hb, cudaStream_t s);
+                     const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active = nullptr,
+                     const int32_t* done = nullptr);
 
 bool agg_eligible(const qc_plan* p) {
   return agg_mode() != 0 && p && p->qc_regular && p->E > 0 && dc_supported(p->L) && dv_supported(p->J) &&
@@ -540,9 +598,11 @@ int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, con
 }
 
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s) {
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active, const int32_t* done) {
   const int vec = pick_vec(lanes);
   AggArgs a = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, lane0, lanes, vec, 0);
+  a.active = active;
+  a.done = done;
   const QcGrid g = make_grid(p);
   switch (p->L) {
     case 4: launch_check_dc<4>(a, vec, from_mu, g, s); break;
@@ -563,10 +623,13 @@ int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const fl
 }
 
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
-                     const float* agg, float* post, uint32_t* hb, cudaStream_t s) {
+                     const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active,
+                     const int32_t* done) {
   const int vec = pick_vec_var(lanes);
   AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
                         agg_reverse());
+  a.active = active;
+  a.done = done;
   const QcGrid g = make_grid(p);
   switch (p->J) {
     case 2: launch_var_dv<2>(a, vec, flags, g, s); break;
@@ -633,6 +696,49 @@ int run_agg_tile(const qc_plan* p, int gamma, int lane0, int lanes, int iters, f
   return 0;
 }
 
+// Early-stop decode (bp.py:242-256) on the compact schedule: the same
+// half-iteration offset between lane halves A and B, plus each half's syndrome
+// and freeze bookkeeping (launch_es_window) right after its variable job;
+// frozen lanes keep packages / posteriors, a half whose lanes are all frozen
+// skips its jobs (done flag).  Decisions, posteriors and iteration counts equal
+// the two-pass early-stop decode (test_compact_early_stop_is_bit_identical).
+// Opt-in (QCB_AGG_ES=1): the two extra control launches per half-iteration
+// make it 7% SLOWER than the two-pass early-stop decode (profiles/r01/
+// kbench_es_compact.jsonl); it pays only once the syndrome and freeze are
+// folded into the fused launch.
+bool agg_es_eligible(const qc_plan* p, int gamma) {
+  static const int v = env_int("QCB_AGG_ES", 0);
+  return v != 0 && agg_fused_eligible(p, gamma);
+}
+
+int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
+                      uint32_t* hb, uint32_t* bad, uint32_t* active, int32_t* done, uint8_t* ok, int32_t* iters_run,
+                      cudaStream_t s) {
+  const int H = gamma / 2, A = 0, B = H;
+  int32_t* dA = done;
+  int32_t* dB = done + 1;
+  int rc;
+  if ((rc = launch_es_start(A, H, iters, bad, active, iters_run, dA, s))) return rc;
+  if ((rc = launch_es_start(B, H, iters, bad, active, iters_run, dB, s))) return rc;
+  if ((rc = launch_agg_check_w(p, gamma, A, H, true, msgs, mu, agg, s, active, dA))) return rc;
+  for (int t = 1; t <= iters; ++t) {
+    const int vflags = AGG_ES | (t == 1 ? AGG_FIRST : 0) | (t == iters ? AGG_LAST : 0);
+    // var(A, t) + check(B, t), then A's syndrome / freeze
+    if ((rc = launch_agg_fused_es(p, gamma, H, A, vflags, B, t == 1, msgs, mu, agg, post, hb, active, dA, dB, s)))
+      return rc;
+    if ((rc = launch_es_window(p, gamma, A, H, t, hb, bad, active, iters_run, dA, s))) return rc;
+    if (t < iters) {
+      // var(B, t) + check(A, t + 1)
+      if ((rc = launch_agg_fused_es(p, gamma, H, B, vflags, A, false, msgs, mu, agg, post, hb, active, dB, dA, s)))
+        return rc;
+    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, active, dB))) {
+      return rc;
+    }
+    if ((rc = launch_es_window(p, gamma, B, H, t, hb, bad, active, iters_run, dB, s))) return rc;
+  }
+  return launch_es_finish(p, gamma, bad, active, ok, post, hb, s);
+}
+
 int agg_decode_launches(const qc_plan* p, int gamma, int iters) {
   const int T = agg_tile_lanes(p, gamma);
   return (gamma / T) * (agg_fused_eligible(p, T) ? 2 * iters + 1 : 2 * iters);
@@ -678,6 +784,8 @@ int qc_agg_fused(const qc_plan* p, int gamma, int lanes, int var_lane0, int var_
 int qc_decode_launches(const qc_plan* p, int gamma, int iters, int early_stop) {
   if (!p || iters < 1) return -1;
   if (!early_stop && qcb::agg_eligible(p)) return 3 + qcb::agg_decode_launches(p, gamma, iters);
+  // compact early stop: 2 es_start, first check, per iteration 2 x (job + syndrome + freeze), finish (2)
+  if (early_stop && qcb::agg_es_eligible(p, gamma)) return 2 + 1 + 6 * iters + 2;
   return early_stop ? 2 + 4 * iters + 2 : 1 + 2 * iters + 2;
 }
 

@@ -55,6 +55,19 @@ __global__ void syndrome_kernel(const uint32_t* hb, uint32_t* bad, const int32_t
   if (par) atomicOr(bad + w, par);
 }
 
+// the same over the 32-lane words [w0, w0 + W) of planes with row stride Wt
+__global__ void syndrome_w_kernel(const uint32_t* hb, uint32_t* bad, const int32_t* check_ptr,
+                                  const int32_t* edge_var, int M, int Wt, int w0, int W, const int32_t* done) {
+  if (done && *done) return;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)M * W) return;
+  int m = (int)(tid / W), w = w0 + (int)(tid - (long long)m * W);
+  int e0 = check_ptr[m], deg = check_ptr[m + 1] - e0;
+  uint32_t par = 0;
+  for (int k = 0; k < deg; ++k) par ^= hb[(size_t)edge_var[e0 + k] * Wt + w];
+  if (par) atomicOr(bad + w, par);
+}
+
 __global__ void hard_bits_kernel(const float* post, uint32_t* hb, int N, int gamma) {
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   int GV = gamma / 4;
@@ -254,6 +267,31 @@ int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* 
 
 namespace qcb {
 int launch_cnu_public(const qc_plan* p, CnuArgs a, int mode, cudaStream_t s) { return launch_cnu(p, a, mode, s); }
+// early-stop bookkeeping on a lane window (compact schedule, agg.cu)
+int launch_es_window(const qc_plan* p, int gamma, int lane0, int lanes, int it, const uint32_t* hb, uint32_t* bad,
+                     uint32_t* active, int32_t* iters_run, int32_t* done, cudaStream_t s) {
+  const int Wt = gamma / 32, w0 = lane0 / 32, W = lanes / 32;
+  if (p->M > 0) {
+    long long threads = (long long)p->M * W;
+    syndrome_w_kernel<<<blocks_for(threads), THREADS, 0, s>>>(hb, bad, p->d_check_ptr, p->d_edge_var, p->M, Wt, w0, W,
+                                                              done);
+  }
+  es_update_kernel<<<1, 256, 0, s>>>(active + w0, bad + w0, iters_run + 32 * w0, done, W, it);
+  return check_launch("es_window");
+}
+int launch_es_start(int lane0, int lanes, int iters, uint32_t* bad, uint32_t* active, int32_t* iters_run,
+                    int32_t* done, cudaStream_t s) {
+  const int w0 = lane0 / 32, W = lanes / 32;
+  es_start_kernel<<<1, 256, 0, s>>>(active + w0, bad + w0, iters_run + 32 * w0, done, W, iters);
+  return check_launch("es_start");
+}
+int launch_es_finish(const qc_plan* p, int gamma, const uint32_t* bad, const uint32_t* active, uint8_t* ok,
+                     const float* post, uint32_t* hb, cudaStream_t s) {
+  finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, active, ok, gamma);
+  long long threads = (long long)p->N * (gamma / 4);
+  hard_bits_kernel<<<blocks_for(threads), THREADS, 0, s>>>(post, hb, p->N, gamma);
+  return check_launch("es_finish");
+}
 int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s) {
   return launch_syndrome(p, gamma, hb, bad, nullptr, s);
 }
@@ -373,6 +411,12 @@ int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const floa
     }
     if ((rc = launch_syndrome(p, gamma, hb, bad, nullptr, s))) return rc;
     finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, nullptr, ok, gamma);
+  } else if (agg_es_eligible(p, gamma)) {
+    // compact schedule with per-lane freezing (agg.cu); done flags per lane half
+    if ((rc = run_agg_decode_es(p, gamma, iters, msgs, mu, reinterpret_cast<float*>(
+                                    work + (2 * (size_t)W + 4 + 63) / 64 * 64),
+                                post, hb, bad, active, done, ok, iters_run, s)))
+      return rc;
   } else {
     es_start_kernel<<<1, 256, 0, s>>>(active, bad, iters_run, done, W, iters);
     for (int it = 1; it <= iters; ++it) {

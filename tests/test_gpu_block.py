@@ -252,6 +252,41 @@ def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
     assert np.array_equal(r4.hard_bits, bits) and np.array_equal(r4.iterations_run, its)
 
 
+_ES_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+import paper_1204_0334_b200 as q
+h, exp = q.load_code(q.codes.bundled_code_path('n18360'))
+lay = q.build_edge_layout(h)
+y = q.simulate_block(q.ChannelConfig(float(sys.argv[2]), 5 / 6, seed=6, gamma=512), lay.n_vars)
+r = q.decode_batch(lay, y, q.ebn0_to_sigma(float(sys.argv[2]), 5 / 6), 30, early_stop=True)
+np.savez(sys.argv[1], post=r.posteriors, bits=r.hard_bits, ok=r.syndrome_ok, its=r.iterations_run)
+"""
+
+
+def test_compact_early_stop_is_bit_identical(gpu, tmp_path):
+    """Early-stop decode on the compact schedule (QCB_AGG_ES=1, default) equals the
+    two-pass early-stop decode bit for bit: posteriors captured at the freeze
+    iteration, hard bits, syndrome flags, iteration counts -- at an SNR where
+    lanes freeze at many different iterations and one where half the frames fail."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for db in ("3.2", "2.9"):
+        outs = []
+        for env in ({"QCB_AGG_ES": "0"}, {"QCB_AGG_ES": "1"}, {"QCB_AGG": "0"}):
+            f = tmp_path / f"es{db}_{len(outs)}.npz"
+            subprocess.run([sys.executable, "-c", _ES_SNIPPET, str(f), db], cwd=repo, check=True,
+                           env={**os.environ, **env})
+            outs.append(np.load(f))
+        its = outs[0]["its"]
+        assert its.min() < its.max()                       # lanes froze at different iterations
+        for o in outs[1:]:
+            for k in ("post", "bits", "ok", "its"):
+                assert np.array_equal(outs[0][k], o[k]), (db, k)
+
+
 def test_graded_chunk_plans_agree(gpu, monkeypatch):
     """The host pipeline's chunk plan (C/4, C/2, C.., remainder, C/4) and its
     per-size graphs give the same DecodeResult for every batch size around the
