@@ -150,3 +150,40 @@ def test_n18360_failing_frames_match_oracle_f64(gpu):
                              stop=2**62, max_frames=128, workers=1)
     assert (g.frames, g.bit_errors, g.frame_errors) == tuple(o)
     assert g.frame_errors > 32
+
+
+def test_multiple_points_use_disjoint_noise(gpu):
+    """test_harness.py:78-84: the same operating point twice draws fresh lanes
+    per point (lane base = point index << 32)."""
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    res = q.run_block_simulation(lay, toy_cfg(q, ebn0_db=[2.0, 2.0]))
+    assert res[0].frames > 0 and res[1].frames > 0
+    assert (res[0].bit_errors, res[0].frame_errors) != (res[1].bit_errors, res[1].frame_errors)
+
+
+def test_stream_counts_match_manual_replay(gpu):
+    """test_harness.py:94-116 through this package's own public API: the device
+    stream campaign counts exactly the push-emitted frames a StreamDecoder fed
+    by lane_normals would count."""
+    import numpy as np
+    q = gpu
+    code = q.unwrap_qc(q.multiplicative_shifts(2, 4, 8))
+    cfg = toy_cfg(q, gamma=2, processors=2, stream_segment_frames=5, stop_block_errors=10**9,
+                  max_frames=20, seed=9)
+    res = q.run_stream_simulation(code, cfg)[0]
+    window = 2 * (code.ms + 1)
+    pushes = 5 + window - 1
+    sigma = q.ebn0_to_sigma(2.0, code.rate_bound)
+    frames = bit_errors = frame_errors = 0
+    for seg in range(2):                      # max_frames consumes exactly two segments
+        dec = q.StreamDecoder(code, 2, gamma=2)
+        for t in range(pushes):
+            y = np.stack([1.0 + sigma * q.lane_normals(9, seg * 2 + g, t * code.c, code.c) for g in range(2)])
+            fr = dec.push_frame(y, sigma)
+            if fr is not None:
+                frames += 2
+                bit_errors += int(fr.hard_bits.sum())
+                frame_errors += int(fr.hard_bits.any(axis=1).sum())
+    assert (res.frames, res.bit_errors, res.frame_errors) == (frames, bit_errors, frame_errors)
+    assert res.iters_or_i == 2
