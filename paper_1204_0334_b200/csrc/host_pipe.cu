@@ -4,10 +4,10 @@
 //
 // A batch of gamma codewords is cut into chunks that rotate over `slots` CUDA
 // streams, each with its own device buffers and instantiated CUDA graphs of
-// the whole flooding loop (qc_decode) for chunk sizes C/4, C/2 and C lanes
-// (C = `chunk`).  The chunk plan ramps C/4, C/2, C, ..., C, C/4: small first
-// and last chunks shorten the pipeline fill (first copy-in) and drain (last
-// copy-out), full-size chunks in between keep the decode kernels at their
+// the whole flooding loop (qc_decode) for chunk sizes C/8, C/4, C/2 and C lanes
+// (C = `chunk`).  The chunk plan ramps up and down through the smaller sizes
+// (C/4, C/2, C, ..., C, C/2, C/4 for C = 512): small first and last chunks
+// shorten the pipeline fill (first copy-in) and drain (last copy-outs), full-size chunks in between keep the decode kernels at their
 // large-gamma efficiency.  Decodes are serialised across streams (event
 // chain): two decodes running concurrently interfere (tools/chain_probe.py);
 // copy-ins are serialised too, so the first chunk is not slowed by later ones
@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -39,8 +41,9 @@ using namespace qcb;
 struct Slot {
   cudaStream_t st = nullptr;
   cudaEvent_t done = nullptr;
-  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};   // C/4, C/2, C lanes
-  int size[3] = {0, 0, 0};
+  static constexpr int NG = 4;
+  cudaGraphExec_t graph[NG] = {};   // C/8, C/4, C/2, C lanes
+  int size[NG] = {};
   cudaEvent_t decoded = nullptr;   // end of this slot's last decode (serialises decodes)
   cudaEvent_t copied_in = nullptr; // end of this slot's last copy-in (serialises copy-ins)
   double* x = nullptr;          // (chunk, N) fp64 lane-major input
@@ -162,8 +165,8 @@ static int init_slot(qc_host_dec* h, Slot& s) {
   HP_CK(cudaMemsetAsync(s.msgs, 0, E * C * sizeof(float), s.st));
   // the flooding loop for each chunk size, captured once and replayed per chunk
   // (a size-c decode uses the slot's buffers with row stride c)
-  for (int i = 0; i < 3; ++i) {
-    const int c = h->chunk >> (2 - i);
+  for (int i = 0; i < Slot::NG; ++i) {
+    const int c = h->chunk >> (Slot::NG - 1 - i);
     if (c < 32 || c % 32) continue;
     s.size[i] = c;
     cudaGraph_t g = nullptr;
@@ -274,33 +277,65 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
   const bool pin_in = pinned(x, (size_t)gamma * row * sizeof(double));
   const int S = (int)h->slots.size();
   const int C = h->chunk;
-  // chunk plan: C/4, C/2, C, ..., C, then the remainder and a final C/4
-  std::vector<int> plan;
-  long long rem = gamma;
-  if (gamma <= C) {
-    plan.push_back(gamma);
-    rem = 0;
-  }
-  for (int c : {C / 4, C / 2})
-    if (c >= 32 && c % 32 == 0 && rem > c + C / 4) {
-      plan.push_back(c);
-      rem -= c;
-    }
-  while (rem > C + C / 4) {
-    plan.push_back(C);
-    rem -= C;
-  }
-  if (rem > C / 4 && C / 4 >= 32 && C % 128 == 0 && !plan.empty()) {
-    plan.push_back((int)(rem - C / 4));
-    plan.push_back(C / 4);
+  // chunk plan: ramp up through the captured sizes from min(128, C/4) lanes
+  // (C/4, C/2 for C = 512), full chunks, then ramp down the same sizes.  Each
+  // ramp step's decode outlasts the next chunk's copy-in (head) or the
+  // previous chunk's copy-out (tail), so only the first copy-in and the last
+  // copy-out stay exposed (QCB_HOST_PROFILE=1 shows the split).
+  std::vector<int> plan, ramp_sizes;
+  const Slot& s0 = h->slots[0];
+  for (int i = 0; i < Slot::NG - 1; ++i)
+    if (s0.size[i] && s0.size[i] >= std::min(128, C / 4)) ramp_sizes.push_back(s0.size[i]);
+  long long ramp_lanes = 0;
+  for (int r : ramp_sizes) ramp_lanes += r;
+  const bool ramp = C % 128 == 0 && C / 4 >= 32;
+  if (!ramp_sizes.empty() && gamma >= 2 * ramp_lanes + C) {
+    long long body = gamma - 2 * ramp_lanes;
+    plan = ramp_sizes;
+    for (; body >= C; body -= C) plan.push_back(C);
+    if (body > 0) plan.push_back((int)body);
+    plan.insert(plan.end(), ramp_sizes.rbegin(), ramp_sizes.rend());
   } else {
-    while (rem > 0) {
-      const int c = (int)std::min<long long>(rem, C);
-      plan.push_back(c);
-      rem -= c;
+    long long rem = gamma;
+    if (gamma <= C) {
+      plan.push_back(gamma);
+      rem = 0;
+    }
+    for (int c : {C / 4, C / 2})
+      if (c >= 32 && c % 32 == 0 && rem > c + C / 4) {
+        plan.push_back(c);
+        rem -= c;
+      }
+    while (rem > C + C / 4) {
+      plan.push_back(C);
+      rem -= C;
+    }
+    if (rem > C / 4 && ramp && !plan.empty()) {
+      plan.push_back((int)(rem - C / 4));
+      plan.push_back(C / 4);
+    } else {
+      while (rem > 0) {
+        const int c = (int)std::min<long long>(rem, C);
+        plan.push_back(c);
+        rem -= c;
+      }
     }
   }
   const long long nchunks = (long long)plan.size();
+  // QCB_HOST_PROFILE=1: per-call breakdown on stderr (decode graph time vs the
+  // whole call on the device clock)
+  static const bool prof = [] {
+    const char* e = std::getenv("QCB_HOST_PROFILE");
+    return e && *e == '1';
+  }();
+  std::vector<cudaEvent_t> pev;
+  auto tev = [&](cudaStream_t st) -> int {
+    cudaEvent_t e;
+    HP_CK(cudaEventCreate(&e));
+    HP_CK(cudaEventRecord(e, st));
+    pev.push_back(e);
+    return 0;
+  };
   cudaEvent_t prev_decoded = nullptr, prev_copied = nullptr;
   long long a = 0;
   for (long long k = 0; k < nchunks; ++k) {
@@ -308,7 +343,7 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     if (int rc = finish(c, s)) return rc;
     const long long b = a + plan[k];
     const int gi = plan[k];
-    int gsel = 2;                                   // smallest captured size holding the chunk
+    int gsel = Slot::NG - 1;                        // smallest captured size holding the chunk
     while (gsel > 0 && s.size[gsel - 1] >= gi) --gsel;
     const int cs = s.size[gsel];
     const double* src = x + (size_t)a * row;
@@ -319,6 +354,7 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     }
     // copy-ins in chunk order, one at a time: the first chunk gets the whole link
     if (prev_copied) HP_CK(cudaStreamWaitEvent(s.st, prev_copied, 0));
+    if (prof && k == 0) tev(s.st);
     HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
     HP_CK(cudaEventRecord(s.copied_in, s.st));
     prev_copied = s.copied_in;
@@ -326,7 +362,9 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     // wait on the previous decode, off the serialised decode chain
     if (int rc = qc_llr_from_lane_major(N, cs, gi, s.x, sigma, s.mu, s.st)) return rc;
     if (prev_decoded) HP_CK(cudaStreamWaitEvent(s.st, prev_decoded, 0));
+    if (prof) tev(s.st);
     HP_CK(cudaGraphLaunch(s.graph[gsel], s.st));
+    if (prof) tev(s.st);
     HP_CK(cudaEventRecord(s.decoded, s.st));
     prev_decoded = s.decoded;
     if (int rc = qc_lane_major(N, cs, gi, s.post, post ? s.post_lm : nullptr, bits ? s.bits_lm : nullptr, s.st))
@@ -354,8 +392,28 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     s.b = b;
     a = b;
   }
+  if (prof) tev(h->slots[(nchunks - 1) % S].st);
   for (long long k = std::max<long long>(0, nchunks - S); k < nchunks; ++k)
     if (int rc = finish(c, h->slots[k % S])) return rc;
+  if (prof) {
+    HP_CK(cudaDeviceSynchronize());
+    float dec = 0.0f, gaps = 0.0f, ms;
+    for (long long k = 0; k < nchunks; ++k) {
+      cudaEventElapsedTime(&ms, pev[1 + 2 * k], pev[2 + 2 * k]);
+      dec += ms;
+      if (k) {
+        cudaEventElapsedTime(&ms, pev[2 * k], pev[1 + 2 * k]);
+        gaps += ms;
+      }
+    }
+    float head, tail, total;
+    cudaEventElapsedTime(&head, pev[0], pev[1]);
+    cudaEventElapsedTime(&tail, pev[2 * nchunks], pev.back());
+    cudaEventElapsedTime(&total, pev[0], pev.back());
+    std::fprintf(stderr, "[qc_host] chunks=%lld decode_ms=%.3f gaps_ms=%.3f head_ms=%.3f tail_ms=%.3f total_ms=%.3f\n",
+                 nchunks, dec, gaps, head, tail, total);
+    for (auto e : pev) cudaEventDestroy(e);
+  }
   return 0;
 }
 

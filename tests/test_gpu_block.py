@@ -288,7 +288,8 @@ def test_compact_early_stop_is_bit_identical(gpu, tmp_path):
 
 
 def test_graded_chunk_plans_agree(gpu, monkeypatch):
-    """The host pipeline's chunk plan (C/4, C/2, C.., remainder, C/4) and its
+    """The host pipeline's chunk plans (C/4, C/2, C.., remainder, C/2, C/4 from
+    2.5 C lanes up; C/4, C/2, C.., remainder, C/4 below) and its
     per-size graphs give the same DecodeResult for every batch size around the
     plan's break points as one single-chunk decode."""
     q = gpu
@@ -299,7 +300,7 @@ def test_graded_chunk_plans_agree(gpu, monkeypatch):
     monkeypatch.setattr(qbp, "HOST_CHUNK", 1024)
     ref = q.decode_batch(lay, y, 0.9, 9)                  # one chunk
     monkeypatch.setattr(qbp, "HOST_CHUNK", 128)
-    for G in (129, 160, 161, 224, 300, 417, 700):
+    for G in (129, 160, 161, 224, 300, 319, 320, 321, 383, 384, 385, 417, 448, 700):
         r = q.decode_batch(lay, y[:G], 0.9, 9)
         for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
             assert np.array_equal(getattr(r, f), getattr(ref, f)[:G]), (G, f)
