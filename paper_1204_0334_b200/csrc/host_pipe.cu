@@ -7,9 +7,10 @@
 // the whole flooding loop (qc_decode) for chunk sizes C/8, C/4, C/2 and C lanes
 // (C = `chunk`).  The chunk plan ramps up and down through the smaller sizes
 // (C/4, C/2, C, ..., C, C/2, C/4 for C = 512): small first and last chunks
-// shorten the pipeline fill (first copy-in) and drain (last copy-outs), full-size chunks in between keep the decode kernels at their
-// large-gamma efficiency.  Decodes are serialised across streams (event
-// chain): two decodes running concurrently interfere (tools/chain_probe.py);
+// shorten the pipeline fill (first copy-in) and drain (last copy-outs),
+// full-size chunks in between keep the decode kernels at their large-gamma
+// efficiency.  Decodes run in chunk order on one decode stream
+// (two decodes running concurrently interfere, tools/chain_probe.py);
 // copy-ins are serialised too, so the first chunk is not slowed by later ones
 // sharing the link; copies in both directions overlap the decodes.  Per chunk:
 //   H2D of the received values (fp64, lane-major)
@@ -44,7 +45,8 @@ struct Slot {
   static constexpr int NG = 4;
   cudaGraphExec_t graph[NG] = {};   // C/8, C/4, C/2, C lanes
   int size[NG] = {};
-  cudaEvent_t decoded = nullptr;   // end of this slot's last decode (serialises decodes)
+  cudaEvent_t decoded = nullptr;   // end of this slot's last decode (on the decode stream)
+  cudaEvent_t ready = nullptr;     // this slot's LLRs converted (decode may start)
   cudaEvent_t copied_in = nullptr; // end of this slot's last copy-in (serialises copy-ins)
   double* x = nullptr;          // (chunk, N) fp64 lane-major input
   float* mu = nullptr;          // (N, chunk) fp32 LLRs
@@ -125,6 +127,7 @@ struct qc_host_dec {
   const qc_plan* plan = nullptr;
   int chunk = 0, iters = 0, early_stop = 0, device = 0;
   std::vector<Slot> slots;
+  cudaStream_t dstream = nullptr;   // every chunk's decode graph, in chunk order
 };
 
 static void free_slot(Slot& s) {
@@ -133,6 +136,7 @@ static void free_slot(Slot& s) {
   if (s.done) cudaEventDestroy(s.done);
   if (s.decoded) cudaEventDestroy(s.decoded);
   if (s.copied_in) cudaEventDestroy(s.copied_in);
+  if (s.ready) cudaEventDestroy(s.ready);
   if (s.st) cudaStreamDestroy(s.st);
   void* dev[] = {s.x, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, s.post_lm, s.bits_lm};
   for (void* d : dev)
@@ -162,6 +166,7 @@ static int init_slot(qc_host_dec* h, Slot& s) {
   HP_CK(cudaMallocHost(&s.h_its, C * sizeof(int32_t)));
   HP_CK(cudaEventCreateWithFlags(&s.decoded, cudaEventDisableTiming));
   HP_CK(cudaEventCreateWithFlags(&s.copied_in, cudaEventDisableTiming));
+  HP_CK(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
   HP_CK(cudaMemsetAsync(s.msgs, 0, E * C * sizeof(float), s.st));
   // the flooding loop for each chunk size, captured once and replayed per chunk
   // (a size-c decode uses the slot's buffers with row stride c)
@@ -205,12 +210,15 @@ int qc_host_create(const qc_plan* plan, int chunk, int slots, int iters, int ear
     return fail_rt("no CUDA device");
   }
   h->slots.resize(slots);
-  for (auto& s : h->slots) {
-    if (int rc = init_slot(h, s)) {
-      for (auto& t : h->slots) free_slot(t);
-      delete h;
-      return rc;
-    }
+  cudaError_t ce = cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking);
+  int rc = ce == cudaSuccess ? 0 : fail_rt(std::string("decode stream: ") + cudaGetErrorString(ce));
+  for (auto& s : h->slots)
+    if (!rc) rc = init_slot(h, s);
+  if (rc) {
+    for (auto& t : h->slots) free_slot(t);
+    if (h->dstream) cudaStreamDestroy(h->dstream);
+    delete h;
+    return rc;
   }
   *out = h;
   return 0;
@@ -219,10 +227,12 @@ int qc_host_create(const qc_plan* plan, int chunk, int slots, int iters, int ear
 void qc_host_destroy(qc_host_dec* h) {
   if (!h) return;
   DeviceGuard g(h->device);
+  if (h->dstream) cudaStreamSynchronize(h->dstream);
   for (auto& s : h->slots) {
     if (s.st) cudaStreamSynchronize(s.st);
     free_slot(s);
   }
+  if (h->dstream) cudaStreamDestroy(h->dstream);
   delete h;
 }
 
@@ -336,7 +346,7 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     pev.push_back(e);
     return 0;
   };
-  cudaEvent_t prev_decoded = nullptr, prev_copied = nullptr;
+  cudaEvent_t prev_copied = nullptr;
   long long a = 0;
   for (long long k = 0; k < nchunks; ++k) {
     Slot& s = h->slots[k % S];
@@ -358,15 +368,16 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
     HP_CK(cudaEventRecord(s.copied_in, s.st));
     prev_copied = s.copied_in;
-    // the LLR conversion only needs this chunk's copy-in: it runs before the
-    // wait on the previous decode, off the serialised decode chain
+    // the LLR conversion only needs this chunk's copy-in; the decode graphs
+    // all run on one stream (no cross-stream hand-off between decodes)
     if (int rc = qc_llr_from_lane_major(N, cs, gi, s.x, sigma, s.mu, s.st)) return rc;
-    if (prev_decoded) HP_CK(cudaStreamWaitEvent(s.st, prev_decoded, 0));
-    if (prof) tev(s.st);
-    HP_CK(cudaGraphLaunch(s.graph[gsel], s.st));
-    if (prof) tev(s.st);
-    HP_CK(cudaEventRecord(s.decoded, s.st));
-    prev_decoded = s.decoded;
+    HP_CK(cudaEventRecord(s.ready, s.st));
+    HP_CK(cudaStreamWaitEvent(h->dstream, s.ready, 0));
+    if (prof) tev(h->dstream);
+    HP_CK(cudaGraphLaunch(s.graph[gsel], h->dstream));
+    if (prof) tev(h->dstream);
+    HP_CK(cudaEventRecord(s.decoded, h->dstream));
+    HP_CK(cudaStreamWaitEvent(s.st, s.decoded, 0));
     if (int rc = qc_lane_major(N, cs, gi, s.post, post ? s.post_lm : nullptr, bits ? s.bits_lm : nullptr, s.st))
       return rc;
     if (post) {
@@ -428,6 +439,7 @@ extern "C" int qc_host_decode(qc_host_dec* h, const double* x, int gamma, double
   DeviceGuard guard(h->device);
   int rc = run(h, x, gamma, sigma, bits, post, ok, iters_run);
   if (rc) {                       // leave no chunk in flight for the next call
+    cudaStreamSynchronize(h->dstream);
     for (auto& s : h->slots) {
       cudaStreamSynchronize(s.st);
       s.a = s.b = -1;
