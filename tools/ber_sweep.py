@@ -5,6 +5,7 @@
 (`run_block_simulation`), optionally sharded over GPUs with torchrun.
 
   python tools/ber_sweep.py --ebn0 2.6 2.8 3.0 3.2 3.4 3.6 --stop 100 --out profiles/r01/ber_n18360.csv
+  python tools/ber_sweep.py --stream 20 --ebn0 ... # LDPCCC (unwrapped code, I = 20 window decoder)
 """
 import argparse
 import os
@@ -23,6 +24,7 @@ def main():
     ap.add_argument("--max-frames", type=int, default=20_000_000)
     ap.add_argument("--gamma-kernel", type=int, default=4096)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--stream", type=int, default=0, help="LDPCCC sweep with this many processors I")
     args = ap.parse_args()
     import paper_1204_0334_b200 as q
     from paper_1204_0334_b200.dist import init_from_env
@@ -32,9 +34,14 @@ def main():
     rows = []
     t0 = time.time()
     for db in args.ebn0:
-        cfg = q.SimulationConfig(code_id=args.code, ebn0_db=[db], iterations=args.iters, gamma=32,
-                                 stop_block_errors=args.stop, max_frames=args.max_frames, seed=0)
-        r = q.run_block_simulation(lay, cfg, gamma_kernel=args.gamma_kernel)[0]
+        if args.stream:
+            cfg = q.SimulationConfig(code_id=args.code + "'", ebn0_db=[db], processors=args.stream, gamma=32,
+                                     stop_block_errors=args.stop, max_frames=args.max_frames, seed=0)
+            r = q.run_stream_simulation(q.unwrap_qc(exp), cfg, gamma_kernel=min(args.gamma_kernel, 512))[0]
+        else:
+            cfg = q.SimulationConfig(code_id=args.code, ebn0_db=[db], iterations=args.iters, gamma=32,
+                                     stop_block_errors=args.stop, max_frames=args.max_frames, seed=0)
+            r = q.run_block_simulation(lay, cfg, gamma_kernel=args.gamma_kernel)[0]
         rows.append(r)
         if rank == 0:
             print(",".join(str(x) for x in r.row()), flush=True)
