@@ -318,7 +318,7 @@ class BlockDecoder:
         return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
 
 
-HOST_CHUNK = 512        # largest pipelined chunk of the host-buffer API (plan C/4, C/2, C.., C/4; tools/e2e_bench.py)
+HOST_CHUNK = 512        # largest pipelined chunk of the host-buffer API (plan C/4, C/2, C.., C/2, C/4; tools/e2e_bench.py)
 HOST_SLOTS = 4          # CUDA streams (device buffer sets) the chunks rotate over, pageable input
 HOST_SLOTS_PINNED = 3   # same for page-locked input (no host staging copy to hide; tools/e2e_bench.py)
 PINNED_MIN_BYTES = 1 << 20

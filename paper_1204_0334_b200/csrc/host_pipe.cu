@@ -21,7 +21,9 @@
 // back, so PCIe (55 GB/s each way on the B200 box, profiles/r01/pcie.json)
 // overlaps the kernels.  Host arrays that are page-locked (cudaHostAlloc /
 // torch pin_memory / cudaHostRegister) are DMA'd in place; pageable arrays go
-// through per-slot pinned staging with a multi-threaded memcpy.
+// through per-slot pinned staging: the staging threads convert them to fp32
+// LLRs on the way (half the staged and PCIe bytes, bit-identical to the device
+// conversion).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -59,7 +61,7 @@ struct Slot {
   double* post_lm = nullptr;    // (chunk, N) fp64 lane-major posteriors
   uint8_t* bits_lm = nullptr;   // (chunk, N) u8 lane-major hard bits
   // page-locked staging (allocated on first use with a pageable array)
-  double* h_in = nullptr;
+  float* h_llr = nullptr;       // (chunk, N) fp32 lane-major LLRs (pageable input, converted on the host)
   double* h_post = nullptr;
   uint8_t* h_bits = nullptr;
   uint8_t* h_ok = nullptr;      // always used (small)
@@ -86,6 +88,69 @@ void par_copy(void* dst, const void* src, size_t bytes) {
     th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, n); });
   }
   for (auto& t : th) t.join();
+}
+
+// Pageable input: the LLR conversion of the device kernel
+// (llr_from_lane_major_kernel, block.cu: mu = clip(2 y / sigma^2, +-50) in
+// fp64, rounded once to fp32) done by the staging threads instead of a plain
+// copy -- the same IEEE operations, so the same bits -- which halves the bytes
+// written to the staging buffer and sent over PCIe.
+// no-trapping-math lets gcc vectorise the compare/selects (divpd, cmppd);
+// results are unchanged (IEEE division, NaN passes both compares unclamped)
+__attribute__((optimize("no-trapping-math"))) void llr_range(float* __restrict dst, const double* __restrict src,
+                                                             size_t lo, size_t hi, double sigma) {
+  const double s2 = sigma * sigma;
+  if (sigma > 0.0) {
+    for (size_t i = lo; i < hi; ++i) {
+      double t = (2.0 * src[i]) / s2;
+      t = t < -50.0 ? -50.0 : t;
+      t = t > 50.0 ? 50.0 : t;
+      dst[i] = static_cast<float>(t);
+    }
+  } else {
+    for (size_t i = lo; i < hi; ++i) {
+      double t = src[i];
+      t = t < -50.0 ? -50.0 : t;
+      t = t > 50.0 ? 50.0 : t;
+      dst[i] = static_cast<float>(t);
+    }
+  }
+}
+
+void par_llr(float* dst, const double* src, size_t n, double sigma) {
+  const size_t MIN_PER_THREAD = size_t(1) << 20;   // elements
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  size_t T = std::min<size_t>({hw, 16, std::max<size_t>(1, n / MIN_PER_THREAD)});
+  auto work = [=](size_t lo, size_t hi) { llr_range(dst, src, lo, hi, sigma); };
+  if (T <= 1) {
+    work(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  size_t per = (n + T - 1) / T;
+  per = (per + 1023) & ~size_t(1023);
+  for (size_t t = 0; t < T; ++t) {
+    const size_t lo = t * per;
+    if (lo >= n) break;
+    th.emplace_back(work, lo, std::min(n, lo + per));
+  }
+  for (auto& t : th) t.join();
+}
+
+// fp32 lane-major LLRs (chunk rows of N) -> variable-major mu (N, gamma);
+// lanes >= gamma_in get the neutral +50 like llr_from_lane_major_kernel
+__global__ void lm32_to_vm_kernel(const float* x, float* mu, int N, int gamma, int gamma_in) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, g0 = blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int g = g0 + dy, n = n0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (g < gamma_in && n < N) ? x[(size_t)g * N + n] : 50.0f;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int n = n0 + dy, g = g0 + threadIdx.x;
+    if (n < N) mu[(size_t)n * gamma + g] = tile[threadIdx.x][dy];
+  }
 }
 
 bool pinned_one(const void* p) {
@@ -141,7 +206,7 @@ static void free_slot(Slot& s) {
   void* dev[] = {s.x, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, s.post_lm, s.bits_lm};
   for (void* d : dev)
     if (d) cudaFree(d);
-  void* host[] = {s.h_in, s.h_post, s.h_bits, s.h_ok, s.h_its};
+  void* host[] = {s.h_llr, s.h_post, s.h_bits, s.h_ok, s.h_its};
   for (void* h : host)
     if (h) cudaFreeHost(h);
   s = Slot{};
@@ -358,19 +423,27 @@ int run(qc_host_dec* h, const double* x, int gamma, double sigma, uint8_t* bits,
     const int cs = s.size[gsel];
     const double* src = x + (size_t)a * row;
     if (!pin_in) {
-      if (!s.h_in) HP_CK(cudaMallocHost(&s.h_in, (size_t)C * row * sizeof(double)));
-      par_copy(s.h_in, src, (size_t)gi * row * sizeof(double));
-      src = s.h_in;
+      if (!s.h_llr) HP_CK(cudaMallocHost(&s.h_llr, (size_t)C * row * sizeof(float)));
+      par_llr(s.h_llr, src, (size_t)gi * row, sigma);
     }
     // copy-ins in chunk order, one at a time: the first chunk gets the whole link
     if (prev_copied) HP_CK(cudaStreamWaitEvent(s.st, prev_copied, 0));
     if (prof && k == 0) tev(s.st);
-    HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
+    if (pin_in)
+      HP_CK(cudaMemcpyAsync(s.x, src, (size_t)gi * row * sizeof(double), cudaMemcpyHostToDevice, s.st));
+    else
+      HP_CK(cudaMemcpyAsync(s.x, s.h_llr, (size_t)gi * row * sizeof(float), cudaMemcpyHostToDevice, s.st));
     HP_CK(cudaEventRecord(s.copied_in, s.st));
     prev_copied = s.copied_in;
     // the LLR conversion only needs this chunk's copy-in; the decode graphs
     // all run on one stream (no cross-stream hand-off between decodes)
-    if (int rc = qc_llr_from_lane_major(N, cs, gi, s.x, sigma, s.mu, s.st)) return rc;
+    if (pin_in) {
+      if (int rc = qc_llr_from_lane_major(N, cs, gi, s.x, sigma, s.mu, s.st)) return rc;
+    } else {
+      lm32_to_vm_kernel<<<dim3((N + 31) / 32, cs / 32), dim3(32, 8), 0, s.st>>>(
+          reinterpret_cast<const float*>(s.x), s.mu, N, cs, gi);
+      HP_CK(cudaGetLastError());
+    }
     HP_CK(cudaEventRecord(s.ready, s.st));
     HP_CK(cudaStreamWaitEvent(h->dstream, s.ready, 0));
     if (prof) tev(h->dstream);

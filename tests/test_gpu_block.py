@@ -252,6 +252,32 @@ def test_pipelined_host_api_matches_single_chunk(gpu, monkeypatch):
     assert np.array_equal(r4.hard_bits, bits) and np.array_equal(r4.iterations_run, its)
 
 
+def test_pageable_llr_staging_matches_pinned(gpu, monkeypatch):
+    """Pageable inputs are converted to fp32 LLRs by the host staging threads,
+    page-locked ones by the device kernel: both must give the same bits,
+    including clip boundaries, huge values, +-0 and the unscaled
+    decode_llr_batch path."""
+    q = gpu
+    from paper_1204_0334_b200 import bp as qbp
+    monkeypatch.setattr(qbp, "HOST_CHUNK", 64)
+    lay = toy(q)
+    rng = np.random.default_rng(9)
+    sigma = 0.7
+    y = rng.normal(1.0, 1.5, size=(200, lay.n_vars))
+    edge = np.array([0.0, -0.0, 1e300, -1e300, 25 * sigma * sigma, -25 * sigma * sigma,
+                     np.nextafter(25 * sigma * sigma, 0), 5e-324, -5e-324, 1e-30])
+    y[0, :edge.size] = edge
+    y[1, :edge.size] = edge[::-1]
+    for fn, arg in ((q.decode_batch, sigma), (q.decode_llr_batch, None)):
+        args = (arg,) if arg is not None else ()
+        monkeypatch.setattr(qbp, "PINNED_MIN_BYTES", 1 << 60)
+        r_page = fn(lay, y, *args, 8)
+        monkeypatch.setattr(qbp, "PINNED_MIN_BYTES", 0)
+        r_pin = fn(lay, q.host_array(y), *args, 8)
+        for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
+            assert np.array_equal(getattr(r_page, f), getattr(r_pin, f)), (fn.__name__, f)
+
+
 _ES_SNIPPET = r"""
 import sys, numpy as np
 sys.path.insert(0, '.')
