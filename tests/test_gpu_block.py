@@ -278,6 +278,27 @@ def test_pageable_llr_staging_matches_pinned(gpu, monkeypatch):
             assert np.array_equal(getattr(r_page, f), getattr(r_pin, f)), (fn.__name__, f)
 
 
+def test_host_pipeline_production_size_matches_device_decoder(gpu):
+    """n18360 at 1500 lanes through decode_batch (default chunk 512: ramp 128,
+    256, full chunks, remainder, 256, 128 over 4 streams, pageable and
+    page-locked input) equals one device BlockDecoder run over all lanes."""
+    q = gpu
+    h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
+    lay = q.build_edge_layout(h)
+    N, M = lay.n_vars, lay.n_checks
+    sigma = q.ebn0_to_sigma(2.9, 1 - M / N)          # waterfall: many failing lanes
+    y = 1.0 + sigma * np.random.default_rng(11).standard_normal((1500, N))
+    dec = q.BlockDecoder(lay, 1500, 30, graph=False, count_bits=False)
+    dec.load_lane_major(y, sigma)
+    dec.run()
+    ref = dec.result(1500)
+    assert 0 < int(ref.syndrome_ok.sum()) < 1500
+    for x in (y, q.host_array(y)):
+        r = q.decode_batch(lay, x, sigma, 30)
+        for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
+            assert np.array_equal(getattr(r, f), getattr(ref, f)), f
+
+
 _ES_SNIPPET = r"""
 import sys, numpy as np
 sys.path.insert(0, '.')
