@@ -63,7 +63,6 @@ def main():
     _lib.call("qc_channel", 0, 0, 0, 0, N, eng.gk, sigma, eng.dec.mu.data_ptr(), None, None, 0)
     out["decode_eager_kbench_llrs_ms"] = timed(lambda i=0: eng.dec._launch())
     out["decode_graph_kbench_llrs_ms"] = timed(lambda i=0: g_dec.replay())
-    import torch as _t
     mu = eng.dec.mu
     out["mu_abs_mean"] = round(float(mu.abs().mean()), 4)
     print(json.dumps(out))
