@@ -18,9 +18,10 @@ def main():
     qbp.HOST_CHUNK = 256
     exp = q.multiplicative_shifts(4, 24, 31)            # (4, 24) grid: fused compact kernels
     lay = q.build_edge_layout(q.expand_qc(exp))
-    cfg = q.ChannelConfig(2.5, 5 / 6, seed=3, gamma=600)
+    cfg = q.ChannelConfig(2.5, 5 / 6, seed=3, gamma=700)
     y = q.simulate_block(cfg, lay.n_vars)                 # on-device channel
-    r = q.decode_batch(lay, y, cfg.sigma, 6)              # host pipeline, 256-lane chunks, ragged tail
+    r = q.decode_batch(lay, y, cfg.sigma, 6)              # host pipeline: 64,128,256,124,128,64 (pageable: host LLRs)
+    q.decode_batch(lay, q.host_array(y), cfg.sigma, 6)    # page-locked input: device LLR conversion
     r2 = q.decode_batch(lay, y[:100], cfg.sigma, 6, early_stop=True)
     assert r.hard_bits.shape == y.shape and r2.iterations_run.max() <= 6
     toy = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
