@@ -80,7 +80,7 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.sw_power_cap,power.draw", "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
@@ -106,8 +106,10 @@ class Clocks:
             for k, nm in enumerate(names):
                 if len(r) > 3 + k and r[3 + k].lower() == "active":
                     reasons.add(nm)
+        pw = [float(r[7]) for r in self.rows if len(r) > 7 and r[7].replace(".", "").isdigit()]
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_mean": round(sum(pw) / len(pw), 1) if pw else None}
 
 
 def code_n18360():
@@ -121,56 +123,99 @@ def algorithmic_bytes_per_codeword(E, N, iters):
     return 4 * (iters * (4 * E + N) + (N + E))
 
 
+def _reference_impl():
+    """'reference' when the real qcldpc is installed in oracle/_ref (oracle/build_ref.py),
+    else 'port' (the oracle's numpy float64 restatement, within a few % of it:
+    profiles/r02/port_vs_reference.json)."""
+    from oracle import build_ref
+    if build_ref.available():
+        if build_ref.site_dir() not in sys.path:
+            sys.path.insert(0, build_ref.site_dir())
+        return "reference"
+    return "port"
+
+
 def cpu_decode_sample(workers: int, batches: int, gamma: int = 32):
-    """Time the oracle (reference algorithm, float64 numpy) on host cores.  The
-    worker pool is spawned (never forked: this process has initialised CUDA and
-    thread pools) and brought up before the timed region."""
+    """Time the reference's CPU decoder on host cores: `batches` gamma-lane
+    batches of n18360 at 30 it, one task per batch, on a pool of `workers`
+    processes -- the reference's own harness tasks (qcldpc.harness._init_block /
+    _block_task, harness.py:137-154) when oracle/_ref holds the real package,
+    else the oracle port.  The pool is spawned (never forked: this process may
+    have initialised CUDA) and brought up before the timed region.
+    Returns (Mbit/s, seconds, frames, kind)."""
     import multiprocessing as mp
-    from oracle import campaign, channel, qc
-    import paper_1204_0334_b200 as q
-    h, exp = q.load_code(q.codes.bundled_code_path("n18360"))
-    lay = qc.qc_layout(exp.shifts, exp.p)
-    sigma = channel.ebn0_to_sigma(EBN0, 1.0 - lay.n_checks / lay.n_vars)
-    kw = dict(lay=lay, seed=0, sigma=sigma, gamma=gamma, iters=ITERS, lane0=0)
+    from paper_1204_0334_b200 import codes as pc
+    kind = _reference_impl()
+    h, exp = pc.load_code(pc.bundled_code_path("n18360"))
+    rate = 1.0 - (exp.block_rows * exp.p) / (exp.block_cols * exp.p)
+    if kind == "reference":
+        import qcldpc
+        from qcldpc.harness import _block_task as task, _init_block as init
+        lay = qcldpc.build_edge_layout(qcldpc.expand_qc(qcldpc.ExponentMatrix(exp.shifts, exp.p)))
+        sigma = qcldpc.ebn0_to_sigma(EBN0, rate)
+        initargs = (lay, qcldpc.SimulationConfig("n18360", [EBN0], iterations=ITERS, gamma=gamma), sigma, 0)
+        ping = abs                                 # picklable no-op task (brings workers up)
+    else:
+        from oracle import campaign, channel, qc
+        lay = qc.qc_layout(exp.shifts, exp.p)
+        sigma = channel.ebn0_to_sigma(EBN0, rate)
+        init, task, ping = campaign._set_ctx, campaign.block_task, campaign.ping
+        initargs = (dict(lay=lay, seed=0, sigma=sigma, gamma=gamma, iters=ITERS, lane0=0),)
     if workers <= 1:
-        campaign._init(**kw)
+        init(*initargs)
         t0 = time.perf_counter()
         for b in range(batches):
-            campaign.block_task(b)
+            task(b)
         dt = time.perf_counter() - t0
     else:
-        with mp.get_context("spawn").Pool(workers, initializer=campaign._set_ctx, initargs=(kw,)) as pool:
-            pool.map(campaign.ping, range(workers), chunksize=1)
+        with mp.get_context("spawn").Pool(workers, initializer=init, initargs=initargs) as pool:
+            pool.map(ping, range(workers), chunksize=1)
             t0 = time.perf_counter()
-            list(pool.imap(campaign.block_task, range(batches)))
+            list(pool.imap(task, range(batches)))
             dt = time.perf_counter() - t0
     frames = batches * gamma
-    return frames * (lay.n_vars - lay.n_checks) / dt / 1e6, dt, frames
+    return frames * (lay.n_vars - lay.n_checks) / dt / 1e6, dt, frames, kind
+
+
+def spawn_ranks(args):
+    """`--gpus N` without torchrun's environment: launch the N ranks ourselves,
+    one process per GPU, exactly as the driver's torchrun command would
+    (127.0.0.1 rendezvous, one node); rank 0 prints the JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd[1:])}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 def run_reference(args):
-    """Reference arm: the reference algorithm's CPU implementation (oracle port of
-    qcldpc.bp, numpy float64 -- the reference is pure Python, nothing to compile)
+    """Reference arm: the reference's own CPU decoder (qcldpc, numpy float64,
+    installed unmodified in oracle/_ref; the oracle port when that is absent)
     on all host cores, same workload (n18360, 30 it, 3.2 dB).  A step is one
     bounded sample: one gamma=32 batch per core decoded in parallel (about 5 s).
     Steps are time-boxed to --ref-budget seconds so any --steps K ends in minutes;
-    the median over completed steps is reported."""
+    the median over completed steps is reported.  Under torchrun only rank 0 works."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
     batches = max(cores, 1)
     cpu_decode_sample(cores, cores)                 # one untimed warm-up sample (pool, caches)
-    vals, t0 = [], time.time()
+    vals, t0, kind = [], time.time(), None
     for _ in range(args.steps):
-        v, dt, frames = cpu_decode_sample(cores, batches)
+        v, dt, frames, kind = cpu_decode_sample(cores, batches)
         vals.append((v, dt))
         if time.time() - t0 > args.ref_budget:
             break
     v = sorted(x[0] for x in vals)[len(vals) // 2]
     ms = sorted(x[1] for x in vals)[len(vals) // 2] * 1e3
-    sample = (f"{batches} batches x 32 codewords of n18360, 30 it, {EBN0} dB, one per core "
-              f"(numpy float64 oracle port of qcldpc.bp)")
+    what = ("qcldpc (the reference package, unmodified, oracle/_ref) harness tasks" if kind == "reference"
+            else "numpy float64 oracle port of qcldpc.bp")
+    sample = f"{batches} batches x 32 codewords of n18360, 30 it, {EBN0} dB, one per core ({what})"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "Mbit/s",
         "n_gpus": 0, "steps": args.steps, "steps_completed": len(vals), "warmup": args.warmup,
@@ -178,7 +223,7 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic (counter-based Philox AWGN, all-zero codeword)",
         "config": {"workload": "n18360 QC-LDPC (4,24,765) block decode, 30 flooding iterations",
                    "gamma": 32, "ebn0_db": EBN0, "host_cores": cores},
-        "cpu_baseline": {"value": round(v, 4), "unit": "Mbit/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": round(v, 4), "unit": "Mbit/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(v, 4), "unit": "Mbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -245,20 +290,39 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=120.0, help="reference arm time box (s)")
+    ap.add_argument("--sustain-s", type=float, default=2.5, help="length of the sustained-rate window (0 = skip)")
+    ap.add_argument("--no-curve", action="store_true", help="skip the decode_batch e2e gamma curve")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
 
     import torch
     import paper_1204_0334_b200 as q
     from paper_1204_0334_b200 import _lib
-    from paper_1204_0334_b200.dist import init_from_env
+    from paper_1204_0334_b200.dist import init_from_env, max_scalar
 
     rank, W, group = init_from_env()
+    if W > 1 and torch.distributed.get_backend() == "nccl" and torch.cuda.device_count() < W:
+        raise SystemExit(f"bench.py: {W} NCCL ranks need {W} GPUs, {torch.cuda.device_count()} visible")
+    if W != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the process group has {W} ranks")
     local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    comm = None
+    if W > 1:
+        # bring the communicator up outside the timed region and say what carries the counters
+        t = torch.ones(1, device="cuda")
+        torch.distributed.all_reduce(t)
+        backend = torch.distributed.get_backend()
+        ver = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None
+        comm = {"backend": backend, "nccl_version": ver, "world_size": W, "ranks_summed": int(t.item()),
+                "devices_visible": torch.cuda.device_count()}
+        print(f"bench.py rank {rank}/{W}: {backend} communicator up on cuda:{local} "
+              f"(nccl {ver}, all_reduce of ones = {int(t.item())})", file=sys.stderr, flush=True)
     lay = code_n18360()
     N, M, E = lay.n_vars, lay.n_checks, lay.edge_count
     K_info = N - M
@@ -290,11 +354,43 @@ def main():
     barrier()
     ms_local = ev0.elapsed_time(ev1)
     ck = clocks.stop()
-    from paper_1204_0334_b200.dist import max_scalar
     ms = max_scalar(ms_local, group, device="cuda")
     frames = args.steps * gamma * W
     value = frames * K_info / (ms / 1e3) / 1e6
     counts = eng.counts.cpu().numpy()
+    # counters of the last timed step summed over ranks: with lanes (step*W + rank)*gamma
+    # a W-rank run covers exactly the lanes of a 1-rank run at W*gamma (tests/test_gpu_dist.py)
+    last = eng.counts.sum(dim=0)
+    if W > 1:
+        torch.distributed.all_reduce(last)
+    last = [int(x) for x in last.cpu()]
+
+    # ---- sustained rate: >= --sustain-s seconds of back-to-back steps (the
+    # board reaches its power cap after ~20 decodes; the headline K steps are
+    # a burst when K is small), with mean board power -> energy per codeword ----
+    sustained = None
+    if args.sustain_s > 0:
+        n_sus = max(args.steps, int(args.sustain_s * 1e3 / (ms / args.steps)) + 1)
+        ck2 = Clocks(local)
+        barrier()
+        ck2.start()
+        time.sleep(0.3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record()
+        for s in range(n_sus):
+            eng.step(lane0(args.warmup + args.steps + s), sigma)
+        e1.record()
+        barrier()
+        sus_ms = max_scalar(e0.elapsed_time(e1), group, device="cuda")
+        c2 = ck2.stop()
+        sus_val = n_sus * gamma * W * K_info / (sus_ms / 1e3) / 1e6
+        pw = c2.get("power_w_mean")
+        sustained = {"value": round(sus_val, 2), "unit": "Mbit/s", "steps": n_sus, "seconds": round(sus_ms / 1e3, 3),
+                     "ms_per_step": round(sus_ms / n_sus, 4), "clocks": c2,
+                     "energy_mj_per_codeword": round(pw * (sus_ms / 1e3) / (n_sus * gamma) * 1e3, 4) if pw else None,
+                     "energy_nj_per_info_bit": round(pw * (sus_ms / 1e3) / (n_sus * gamma * K_info) * 1e9, 3)
+                     if pw else None}
 
     # ---- dominant kernel: the fused half-iteration kernel of the compact
     # schedule (variable job on one lane half + check job on the other; 2 x 30 - 1
@@ -393,6 +489,23 @@ def main():
                "steps": e_steps,
                "pageable_input_value": e2e_rate(y_pageable, max(2, e_steps // 2))}
         del y, y_pageable
+        # decode_batch e2e over the batch size a caller passes (page-locked y), N=1 only
+        if not args.no_curve and W == 1:
+            curve = []
+            for G in (32, 64, 128, 512, 4096):
+                yg = q.host_array(1.0 + sigma * rng.standard_normal((G, N)))
+                for _ in range(2):
+                    q.decode_batch(lay, yg, sigma, ITERS)
+                torch.cuda.synchronize()
+                n_calls, t0 = 0, time.perf_counter()
+                while n_calls < 3 or time.perf_counter() - t0 < 0.5:
+                    q.decode_batch(lay, yg, sigma, ITERS)
+                    n_calls += 1
+                dt = time.perf_counter() - t0
+                curve.append({"gamma": G, "mbit_s": round(n_calls * G * K_info / dt / 1e6, 2),
+                              "ms_per_call": round(dt / n_calls * 1e3, 3)})
+                del yg
+            e2e["gamma_curve"] = curve
 
     stream = stream_bench(args, q, rank, W, group, barrier) if args.stream_gamma else None
 
@@ -400,10 +513,12 @@ def main():
     if rank == 0 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
         nb = args.cpu_batches or cores
-        v, dt, fr = cpu_decode_sample(cores, nb)
-        cpu = {"value": round(v, 4), "unit": "Mbit/s", "cores": cores, "kind": "port",
+        v, dt, fr, kind = cpu_decode_sample(cores, nb)
+        what = ("the reference package qcldpc (unmodified, oracle/_ref), its harness tasks" if kind == "reference"
+                else "numpy float64 oracle port of qcldpc.bp")
+        cpu = {"value": round(v, 4), "unit": "Mbit/s", "cores": cores, "kind": kind,
                "sample": f"{fr} codewords ({nb} x gamma=32 batches) of n18360 at 30 it, {dt:.1f} s, "
-                         f"numpy float64 oracle port of qcldpc.bp on {cores} processes"}
+                         f"{what} on {cores} processes"}
 
     if rank == 0:
         print(json.dumps({
@@ -415,7 +530,9 @@ def main():
                        "gamma": gamma, "ebn0_db": EBN0, "iterations": ITERS,
                        "parallelism": f"dp{W} (independent codeword batches)",
                        "l2": f"message store {E * gamma * 4 / 1e6:.0f} MB vs 126 MB L2 (inputs larger than L2)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sustained": sustained,
+            "counts_last_step": {"frames": last[0], "bit_errors": last[1], "frame_errors": last[2]},
+            "communicator": comm,
             "gpu_launches": eng.kernel_launches_per_step() * args.steps,
             "stream": stream,
             "clocks": ck,
@@ -426,4 +543,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -63,8 +63,10 @@ QC_API int qc_init(const qc_plan* plan, int gamma, const float* mu, float* msgs,
  * words or NULL (all lanes). */
 QC_API int qc_cnu(const qc_plan* plan, int gamma, float* msgs, const uint32_t* active,
            void* stream);
-/* variable_node_update (bp.py:165-188): msgs <- beta, post (N,gamma) <- clip(total)
- * (post may be NULL); hb (N,gamma/32) hard-bit planes of post (may be NULL). */
+/* variable_node_update (bp.py:165-188): msgs <- beta on active lanes (frozen
+ * lanes keep their packages, bp.py:185-186), post (N,gamma) <- clip(total) on
+ * EVERY lane (bp.py:183; post may be NULL); hb (N,gamma/32) hard-bit planes of
+ * post (may be NULL). */
 QC_API int qc_vnu(const qc_plan* plan, int gamma, float* msgs, const float* mu, float* post,
            uint32_t* hb, const uint32_t* active, void* stream);
 /* The same passes in the representation used inside qc_decode:

@@ -34,51 +34,79 @@ def init_buffer(lay, mu_vg):
 
 
 def _excl_prod(t):
-    """Exclusive products along axis 1, fixed sequential order (bp.py:120-131)."""
+    """Exclusive products along axis 1, fixed sequential order, written in
+    place with np.multiply(out=) exactly as bp.py:120-131 does (same floats,
+    same memory traffic as the reference)."""
     d = t.shape[1]
-    f = np.ones_like(t)
-    b = np.ones_like(t)
+    f = np.empty_like(t)
+    b = np.empty_like(t)
+    f[:, 0] = 1.0
     for k in range(1, d):
-        f[:, k] = f[:, k - 1] * t[:, k - 1]
+        np.multiply(f[:, k - 1], t[:, k - 1], out=f[:, k])
+    b[:, d - 1] = 1.0
     for k in range(d - 2, -1, -1):
-        b[:, k] = b[:, k + 1] * t[:, k + 1]
+        np.multiply(b[:, k + 1], t[:, k + 1], out=b[:, k])
     return f * b
 
 
+def _regular_degree(lay):
+    """d when every check has degree d (row-major edge ids: check m owns edges
+    m*d .. m*d+d-1, so the (E, gamma) buffer reshapes to (M, d, gamma) without
+    a gather -- the reference's check_regular path, codes.py:239-247)."""
+    d = lay.check_pad.shape[1] if lay.check_pad.ndim == 2 else 0
+    return d if d and lay.n_checks * d == lay.edge_count else None
+
+
 def check_update(buf, lay, active=None):
+    """bp.py:134-162 (regular codes reshape, irregular ones gather check_pad)."""
     if lay.edge_count == 0:
         return
     t = np.tanh(0.5 * buf)
     t[-1] = 1.0
-    g = t[lay.check_pad]                              # (M, dc, gamma)
-    pr = np.clip(_excl_prod(g), -1.0 + TANH_CLAMP, 1.0 - TANH_CLAMP)
-    a = np.clip(2.0 * np.arctanh(pr), -L_MAX, L_MAX)
+    d = _regular_degree(lay)
+    g = t[:-1].reshape(lay.n_checks, d, buf.shape[1]) if d else t[lay.check_pad]
+    pr = _excl_prod(g)
+    np.clip(pr, -1.0 + TANH_CLAMP, 1.0 - TANH_CLAMP, out=pr)
+    a = 2.0 * np.arctanh(pr)
+    np.clip(a, -L_MAX, L_MAX, out=a)
     if active is not None:
-        a = np.where(active, a, buf[lay.check_pad])
-    buf[lay.check_pad] = a
-    buf[-1] = 0.0
+        old = buf[:-1].reshape(a.shape) if d else buf[lay.check_pad]
+        a = np.where(active, a, old)
+    if d:
+        buf[:-1] = a.reshape(lay.edge_count, buf.shape[1])
+    else:
+        buf[lay.check_pad] = a
+        buf[-1] = 0.0
 
 
 def var_update(buf, mu_vg, lay, active=None):
+    """bp.py:165-188: running total in increasing edge order, in place."""
     a = buf[lay.var_pad]                              # (N, dv, gamma), pads read 0
     tot = mu_vg.copy()
     for k in range(a.shape[1]):
-        tot = tot + a[:, k]
+        tot += a[:, k]
     beta = np.clip(tot[:, None, :] - a, -L_MAX, L_MAX)
+    post = np.clip(tot, -L_MAX, L_MAX)
     if active is not None:
         beta = np.where(active, beta, a)
     buf[lay.var_pad] = beta
     buf[-1] = 0.0
-    return np.clip(tot, -L_MAX, L_MAX)
+    return post
 
 
 def hd_syndrome(lay, post_vg):
+    """bp.py:191-210."""
     bits = (post_vg < 0).astype(np.uint8)
     if lay.edge_count == 0:
         return bits, np.ones(post_vg.shape[1], bool)
-    eb = np.concatenate([bits[lay.edge_var], np.zeros((1, bits.shape[1]), np.uint8)])
-    par = eb[lay.check_pad].sum(axis=1) & 1
-    return bits, ~par.any(axis=0)
+    eb = bits[lay.edge_var]
+    d = _regular_degree(lay)
+    if d:
+        par = eb.reshape(lay.n_checks, d, -1).sum(axis=1)
+    else:
+        eb = np.concatenate([eb, np.zeros((1, bits.shape[1]), np.uint8)])
+        par = eb[lay.check_pad].sum(axis=1)
+    return bits, ~np.any(par & 1, axis=0)
 
 
 def decode_llr(lay, mu, iterations, early_stop=False):

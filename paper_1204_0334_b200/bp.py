@@ -21,6 +21,7 @@ outputs in HBM) used by the campaign drivers and the float64 build.
 from __future__ import annotations
 
 import dataclasses
+import os
 import threading
 
 import numpy as np
@@ -33,6 +34,7 @@ __all__ = [
     "L_MAX", "TANH_CLAMP", "MessageBatch", "DecodeResult", "channel_llrs", "init_messages",
     "check_node_update", "variable_node_update", "hard_decision_and_syndrome",
     "decode_llr_batch", "decode_batch", "BlockDecoder", "HostDecoder", "host_array",
+    "set_pinned_outputs", "release_pinned_cache",
 ]
 
 L_MAX = 50.0
@@ -51,8 +53,14 @@ def _stream():
 class MessageBatch:
     """Per-edge message packages of gamma lock-step codewords, resident on the GPU.
 
-    `packages` returns a float64 host copy shaped (E, gamma) like the
-    reference; `packages_device` is the live (E, gamma) fp32 device view.
+    `packages` behaves like the reference's writable (E, gamma) float64 view
+    (bp.py:82-84): the first access copies the device store into a host
+    mirror; later accesses return the same array (O(1), so per-edge loops such
+    as test_acceptance.py:207 stay cheap).  While a mirror exists the updates
+    are write-through: check_node_update / variable_node_update upload it
+    first (caller writes take effect) and refresh it in place afterwards, so a
+    held reference sees the new packages exactly as a numpy view would.
+    `packages_device` is the live (E, gamma) device view (no copies).
     """
 
     def __init__(self, layout: EdgeLayout, mu: np.ndarray):
@@ -65,6 +73,7 @@ class MessageBatch:
         self.mu = mu
         self._gp = pad32(self.gamma)
         self.fp64 = get_precision() == "float64"
+        self._host = None
         dt = torch.float64 if self.fp64 else torch.float32
         dev = torch.device("cuda", torch.cuda.current_device())
         m = torch.full((layout.n_vars, self._gp), L_MAX, dtype=dt)
@@ -81,7 +90,21 @@ class MessageBatch:
 
     @property
     def packages(self) -> np.ndarray:
-        return self.packages_device.double().cpu().numpy()
+        if self._host is None:
+            self._host = self.packages_device.double().cpu().numpy()
+        return self._host
+
+    def _before_update(self):
+        """Push caller writes made through the host mirror to the device."""
+        if self._host is not None:
+            import torch
+            self.packages_device.copy_(torch.from_numpy(self._host))
+
+    def _after_update(self):
+        """Refresh the host mirror in place (view semantics)."""
+        if self._host is not None:
+            import torch
+            torch.from_numpy(self._host).copy_(self.packages_device.double())
 
 
 @dataclasses.dataclass
@@ -114,19 +137,25 @@ def check_node_update(batch: MessageBatch, layout: EdgeLayout, active: np.ndarra
     if layout.edge_count == 0:
         return
     act = _active_dev(active, batch._gp)
+    batch._before_update()
     _lib.call("qc64_cnu" if batch.fp64 else "qc_cnu", layout.plan().handle, batch._gp,
               batch._msgs.data_ptr(), _lib.ptr(act), _stream())
+    batch._after_update()
 
 
 def variable_node_update(batch: MessageBatch, layout: EdgeLayout,
                          active: np.ndarray | None = None) -> np.ndarray:
-    """Packages <- variable-to-check messages; returns posteriors (N, gamma) (bp.py:165-188)."""
+    """Packages <- variable-to-check messages on active lanes; returns the
+    posteriors clip(mu + sum alpha) of EVERY lane, frozen ones included
+    (N, gamma) (bp.py:165-188)."""
     import torch
     act = _active_dev(active, batch._gp)
     post = torch.zeros((layout.n_vars, batch._gp), dtype=batch._msgs.dtype, device=batch._msgs.device)
+    batch._before_update()
     _lib.call("qc64_vnu" if batch.fp64 else "qc_vnu", layout.plan().handle, batch._gp,
               batch._msgs.data_ptr(), batch._mu_dev.data_ptr(), post.data_ptr(), None,
               _lib.ptr(act), _stream())
+    batch._after_update()
     return post[:, : batch.gamma].double().cpu().numpy()
 
 
@@ -198,6 +227,7 @@ class BlockDecoder:
         self._graph = None
         self._x = None          # lane-major fp64 staging (device)
         self._host = {}         # pinned host buffers
+        self._lock = threading.Lock()
 
     # -- device work ------------------------------------------------------
     def _launch(self):
@@ -360,12 +390,31 @@ class HostDecoder:
         return DecodeResult(hard_bits=bits, posteriors=post, syndrome_ok=ok, iterations_run=its)
 
 
+_PINNED_OUTPUTS = [os.environ.get("QCLDPC_B200_PINNED_OUTPUTS", "1") != "0"]
+
+
+def set_pinned_outputs(on: bool) -> None:
+    """Whether decode_batch / decode_llr_batch return large results in page-locked
+    memory (default on: the device DMAs straight into them, ~10% faster e2e).
+    Page-locked blocks come from torch's caching host allocator: a dropped
+    result's block is reused by the next call but stays pinned for the life
+    of the process; release_pinned_cache() returns the unused ones to the OS."""
+    _PINNED_OUTPUTS[0] = bool(on)
+
+
+def release_pinned_cache() -> None:
+    """Free the cached page-locked blocks no live result array uses."""
+    import torch
+    torch._C._host_emptyCache()
+
+
 def host_empty(shape, dtype) -> np.ndarray:
     """Output array for the host-buffer API: large ones come from torch's caching
-    page-locked allocator, so the decoder DMAs straight into them and a freed
-    result's pages are reused by the next call (no fresh page faults)."""
+    page-locked allocator (unless set_pinned_outputs(False)), so the decoder
+    DMAs straight into them and a freed result's pages are reused by the next
+    call (no fresh page faults)."""
     dtype = np.dtype(dtype)
-    if int(np.prod(shape)) * dtype.itemsize < PINNED_MIN_BYTES:
+    if not _PINNED_OUTPUTS[0] or int(np.prod(shape)) * dtype.itemsize < PINNED_MIN_BYTES:
         return np.empty(shape, dtype=dtype)
     import torch
     tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
@@ -417,9 +466,10 @@ def _decode_host(layout: EdgeLayout, x: np.ndarray, sigma: float | None, iterati
     require_cuda()
     if get_precision() == "float64":
         dec = _decoder(layout, x.shape[0], iterations, early_stop)
-        dec.load_lane_major(x, sigma)
-        dec.run()
-        return dec.result(x.shape[0])
+        with dec._lock:                    # one call at a time per cached decoder (shared buffers)
+            dec.load_lane_major(x, sigma)
+            dec.run()
+            return dec.result(x.shape[0])
     x = np.ascontiguousarray(x, dtype=np.float64)
     pinned = bool(x.size) and _lib.load().qc_host_is_pinned(x.ctypes.data, x.nbytes) == 1
     return _host_decoder(layout, x.shape[0], iterations, early_stop, pinned).decode(x, sigma or 0.0)

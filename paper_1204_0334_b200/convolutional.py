@@ -117,21 +117,70 @@ class StreamDecoder:
         self._mu = torch.empty((code.c, self._gp), dtype=torch.float32, device=dev)
         self._post = torch.zeros((code.c, self._gp), dtype=torch.float32, device=dev)
         self._y = torch.empty((gamma, code.c), dtype=torch.float64, device=dev)
+        self._kind = np.zeros((processors, code.lam * code.lam), dtype=np.int8)
+        self._ring_live = np.zeros(self.window, dtype=bool)
+
+    # What each (processor group, sub-block label) block of the message store
+    # holds in the REFERENCE's terms after the slots run so far (host-side
+    # bookkeeping of convolutional.py:256-334, O(I*T) per slot): the device
+    # keeps var->check messages in phi form and skips the emission-time clear
+    # (convolutional.py:328-330), so message_memory / channel_memory translate.
+    _ZERO, _BETA, _ALPHA = 0, 1, 2
+
+    def _track(self, t):
+        code, T, I, kind = self.code, self.period, self.processors, self._kind
+        ph = t % T
+        for d in range(T):
+            kind[(t // T) % I, code.lut_v[ph, d]] = self._BETA
+        self._ring_live[t % self.window] = True
+        for i in range(1, I + 1):
+            s = t - (i - 1) * T
+            if s < 0:
+                break
+            for d in range(T):
+                f = s - code.ms + d
+                if f >= 0:
+                    kind[(f // T) % I, code.lut_c[ph, d]] = self._ALPHA
+        for i in range(1, I + 1):
+            j = t - i * T + 1
+            if j < 0:
+                break
+            for d in range(T):
+                kind[(j // T) % I, code.lut_v[j % T, d]] = self._BETA if i < I else self._ZERO
+            if i == I:
+                self._ring_live[j % self.window] = False
 
     @property
     def channel_memory(self) -> np.ndarray:
-        """Channel LLR ring, (I*(m_s+1), c, gamma)."""
-        return self._ring[:, :, : self.gamma].double().cpu().numpy()
+        """Channel LLR ring, (I*(m_s+1), c, gamma) float64 host copy; slots of
+        emitted frames read 0.0 as in the reference (convolutional.py:331)."""
+        ring = self._ring[:, :, : self.gamma].double().cpu().numpy()
+        ring[~self._ring_live] = 0.0
+        return ring
 
     @property
     def message_memory(self) -> np.ndarray:
-        """Edge message packages, (I, base edge count, gamma).
-
-        Internal representation: check->variable packages hold alpha as in the
-        reference; variable->check packages hold sign(beta) * phi(|beta|) / ln 2
-        (the "phi form" the check kernel consumes), not beta itself."""
+        """Edge message packages, (I, base edge count, gamma) float64 host copy,
+        in the reference's representation (convolutional.py:200-218): alpha on
+        check->variable blocks, beta on variable->check blocks (converted from
+        the device's phi form, beta = sign * phi(|psi| ln 2), within fp32
+        rounding), 0.0 on never-written / emitted blocks."""
+        code = self.code
         m = self._msg[:, : self.gamma].double().cpu().numpy()
-        return m.reshape(self.processors, self.code.edge_count, self.gamma)
+        m = m.reshape(self.processors, code.edge_count, self.gamma)
+        for g in range(self.processors):
+            for lbl in range(code.lam * code.lam):
+                sl = slice(int(code.sub_offset[lbl]), int(code.sub_offset[lbl] + code.sub_edge_count[lbl]))
+                k = self._kind[g, lbl]
+                if k == self._ZERO:
+                    m[g, sl] = 0.0
+                elif k == self._BETA:
+                    psi = m[g, sl]
+                    x = np.abs(psi) * math.log(2.0)
+                    with np.errstate(divide="ignore", over="ignore"):
+                        mag = -np.log(np.tanh(0.5 * x))          # phi is its own inverse
+                    m[g, sl] = np.copysign(np.minimum(mag, 50.0), psi)
+        return m
 
     def push_frame(self, y_frame: np.ndarray, sigma: float) -> DecodedFrame | None:
         """Feed one received frame (gamma, c); return the emitted frame or None."""
@@ -151,6 +200,12 @@ class StreamDecoder:
         """B200 extension: push a frame of LLRs already on the device, (c, gamma_pad) fp32."""
         if self._flushed:
             raise RuntimeError("decoder already flushed; create a new one")
+        import torch
+        if (not isinstance(mu_dev, torch.Tensor) or mu_dev.dtype != torch.float32 or not mu_dev.is_cuda
+                or mu_dev.device != self._msg.device or tuple(mu_dev.shape) != (self.code.c, self._gp)
+                or not mu_dev.is_contiguous()):
+            raise ValueError(f"mu_dev must be a contiguous float32 tensor of shape {(self.code.c, self._gp)} "
+                             f"on {self._msg.device}")
         return self._advance(mu_dev, tail=False)
 
     def flush(self) -> list:
@@ -168,6 +223,7 @@ class StreamDecoder:
     def _advance(self, mu_dev, tail: bool) -> DecodedFrame | None:
         t = self.t
         j = t - self.window + 1
+        self._track(t)
         _lib.call("cc_slot", self._plan.handle, self.processors, self._gp, t, None,
                   self._msg.data_ptr(), self._ring.data_ptr(), _lib.ptr(mu_dev),
                   self._post.data_ptr() if j >= 0 else None, None, _lib.stream_handle())

@@ -328,6 +328,7 @@ int qc_vnu(const qc_plan* p, int gamma, float* msgs, const float* mu, float* pos
   VnuArgs a{};
   a.msgs = msgs; a.mu = mu; a.post = post; a.hb = hb; a.active = active; a.done = nullptr;
   a.gamma = gamma;
+  a.post_all = 1;   // frozen lanes keep their packages but still get clip(total) (bp.py:183-187)
   return launch_vnu(p, a, VNU_BETA, as_stream(stream));
 }
 

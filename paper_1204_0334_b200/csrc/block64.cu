@@ -69,9 +69,12 @@ __global__ void __launch_bounds__(THREADS) vnu64_kernel(double* msgs, const doub
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = tid < (long long)N * gamma;
   int n = valid ? (int)(tid / gamma) : 0, g = valid ? (int)(tid - (long long)n * gamma) : 0;
+  // write_beta bit 0: write beta packages (active lanes only); bit 1: posteriors
+  // for every lane, frozen ones included (public single step, bp.py:183)
   bool on = valid && lane_on(active, g);
+  bool calc = valid && (on || (write_beta & 2));
   unsigned bit = 0;
-  if (on) {
+  if (calc) {
     int e[DV];
     double a[DV];
     double tot = mu[(size_t)n * gamma + g];
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(THREADS) vnu64_kernel(double* msgs, const doub
       a[j] = e[j] >= 0 ? msgs[(size_t)e[j] * gamma + g] : 0.0;
       tot = __dadd_rn(tot, a[j]);        // pads add 0.0 (bp.py:227-230)
     }
-    if (write_beta) {
+    if (on && (write_beta & 1)) {
 #pragma unroll
       for (int j = 0; j < DV; ++j)
         if (e[j] >= 0) msgs[(size_t)e[j] * gamma + g] = clampd(__dsub_rn(tot, a[j]), L_MAX64);
@@ -263,7 +266,7 @@ int qc64_vnu(const qc_plan* p, int gamma, double* msgs, const double* mu, double
              const uint32_t* active, void* stream) {
   if (int r = gamma_ok(gamma)) return r;
   if (!p || !msgs || !mu) return fail_arg("null argument");
-  return launch_vnu64(p, msgs, mu, post, hb, active, nullptr, gamma, 1, as_stream(stream));
+  return launch_vnu64(p, msgs, mu, post, hb, active, nullptr, gamma, 3, as_stream(stream));
 }
 
 int qc64_hard_bits(const qc_plan* p, int gamma, const double* post, uint32_t* hb, void* stream) {

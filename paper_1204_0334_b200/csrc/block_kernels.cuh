@@ -60,6 +60,7 @@ struct VnuArgs {
   const uint32_t* active;
   const int32_t* done;
   int N, gamma, dv;
+  int post_all;              // posteriors for every lane, frozen ones too (public single step, bp.py:183)
 };
 
 // Check-node update on registers: x[k][i] (edge k, lane i) -> alpha.
@@ -169,7 +170,10 @@ __global__ void __launch_bounds__(THREADS) cnu_kernel(CnuArgs a, const __grid_co
       }
     }
   }
-  cnu_core<DC, VEC, MODE == CNU_PHI>(x, deg, lanes);
+  // the public single step (beta in) takes the relative-accurate check-side phi
+  // (|alpha| within ~1e-5 relative down to tiny alphas); inside the decode loop
+  // the absolute-accurate grade suffices (alpha only enters sums)
+  cnu_core<DC, VEC, MODE == CNU_PHI, MODE == CNU_BETA>(x, deg, lanes);
 #pragma unroll
   for (int k = 0; k < DC; ++k)
     if (k < deg) vstore<VEC>(a.msgs + (size_t)(e0 + k) * a.gamma + q * VEC, x[k]);
@@ -205,7 +209,8 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
   }
   float tot[VEC], am[DV][VEC];
   unsigned bits = 0;
-  if (valid && lanes) {
+  const unsigned plane = a.post_all ? (1u << VEC) - 1u : lanes;   // lanes whose posterior is written
+  if (valid && plane) {
     vload<VEC>(a.mu + (size_t)n * a.gamma + q * VEC, tot);
 #pragma unroll
     for (int j = 0; j < DV; ++j)
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
 #pragma unroll
         for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], am[j][i]);
       }
-    if constexpr (MODE != VNU_NONE) {
+    if (MODE != VNU_NONE && lanes) {
 #pragma unroll
       for (int j = 0; j < DV; ++j)
         if (j < deg) {
@@ -256,11 +261,11 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
       bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
     }
     if (a.post) {
-      if (lanes == (1u << VEC) - 1u) {
+      if (plane == (1u << VEC) - 1u) {
         vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
       } else {
         for (int i = 0; i < VEC; ++i)
-          if ((lanes >> i) & 1u) a.post[(size_t)n * a.gamma + q * VEC + i] = pst[i];
+          if ((plane >> i) & 1u) a.post[(size_t)n * a.gamma + q * VEC + i] = pst[i];
       }
     }
   }

@@ -35,7 +35,7 @@ from .channel import ebn0_to_sigma, seed_words
 from .codes import EdgeLayout
 from .convolutional import LdpcccCode
 from .dist import ordered_prefix, sum_counts, world
-from .plan import require_cuda
+from .plan import pad32, require_cuda
 
 __all__ = [
     "SimulationConfig", "PointResult", "CSV_COLUMNS", "run_block_simulation",
@@ -134,6 +134,50 @@ def _kernel_units(gref: int, target_lanes: int, max_units: int) -> int:
     return max(step, -(-want // step) * step)
 
 
+def _run_rounds(step, counts_of, units: int, frames_per_unit: int, rank: int, W: int, group,
+                stop: int, max_frames: int):
+    """Drive rounds of a campaign engine until the reference's ordered stop rule
+    holds (harness.py:173-192); returns (frames, bit_errors, frame_errors).
+
+    Round k: `step(k)` decodes this rank's `units` reference batches, their
+    counters land in rank's slice of a (W * units, 3) array, one all_reduce(SUM)
+    merges the ranks (NCCL on GPUs), and the array is copied to page-locked
+    memory behind an event -- all stream-ordered, nothing blocks the host.
+    Round k + 1 is queued BEFORE round k's counters are read, so the device
+    never idles while the host applies the stop rule.  The look-ahead round is
+    only queued while the frame budget is not already exhausted by the rounds in
+    flight; when a frame-error stop lands, its (uncounted) work is discarded --
+    the counts are those of the ordered prefix, as with the reference's pool.
+    """
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    per_round = W * units * frames_per_unit
+
+    def launch(rnd):
+        step(rnd)
+        allc = torch.zeros((W * units, 3), dtype=torch.int64, device=dev)
+        allc[rank * units:(rank + 1) * units] = counts_of()
+        sum_counts(allc, group)
+        host = torch.empty((W * units, 3), dtype=torch.int64, pin_memory=True)
+        host.copy_(allc, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return host, ev
+
+    tot, rnd = (0, 0, 0), 0
+    cur = launch(0)
+    while True:
+        # rounds 0..rnd are queued; speculate on rnd + 1 unless the budget ends earlier
+        nxt = launch(rnd + 1) if (rnd + 1) * per_round < max_frames else None
+        host, ev = cur
+        ev.synchronize()
+        tot, done, _ = ordered_prefix(host.numpy(), stop, max_frames, tot)
+        if done:
+            return tot
+        rnd += 1
+        cur = nxt if nxt is not None else launch(rnd)
+
+
 class BlockCampaign:
     """Device-resident block campaign engine for one code / gamma_kernel / iteration count."""
 
@@ -141,7 +185,7 @@ class BlockCampaign:
                  early_stop: bool, seed: int, graph: bool = True):
         torch = require_cuda()
         self.layout, self.gref, self.units = layout, gamma_ref, units
-        self.gk = gamma_ref * units
+        self.gk = gamma_ref * units             # counted lanes; the kernels run pad32(gk)
         self.k0, self.k1 = seed_words(seed)
         # campaigns run the fp32 production kernels (the channel writes fp32 LLRs)
         self.dec = BlockDecoder(layout, self.gk, iterations, early_stop, graph=False, count_bits=True,
@@ -156,7 +200,7 @@ class BlockCampaign:
     def _launch(self):
         n = self.layout.n_vars
         self.counts.zero_()
-        _lib.call("qc_channel_dev", self.k0, self.k1, self.lane0.data_ptr(), 0, n, self.gk,
+        _lib.call("qc_channel_dev", self.k0, self.k1, self.lane0.data_ptr(), 0, n, self.dec.gp,
                   float(self.sigma), self.dec.mu.data_ptr(), _lib.stream_handle())
         self.dec._launch()
         _lib.call("qc_batch_counts", self.gk, self.gref, self.dec.lane_bits.data_ptr(),
@@ -166,7 +210,9 @@ class BlockCampaign:
         return 1 + self.dec.kernel_launches_per_run() + 1
 
     def step(self, lane0: int, sigma: float):
-        """Decode lanes lane0 .. lane0 + gamma_kernel - 1; counts -> self.counts (device)."""
+        """Decode lanes lane0 .. lane0 + gamma_kernel - 1; counts -> self.counts (device).
+        (When gamma_kernel is not a multiple of 32 the padding lanes decode the
+        next lane ids too, but only the first gamma_kernel lanes are counted.)"""
         import torch
         self.lane0.fill_(int(lane0))
         if self.sigma != sigma:
@@ -234,10 +280,12 @@ class RecycleCampaign:
         counts = torch.zeros((n_batches + W, 3), dtype=torch.int64, device=self.mu.device)
         _lib.call("qc_rc_init", self.gk, int(id_limit), self.state.data_ptr(), _lib.stream_handle())
         self._graph = None
-        tot, done, scan = (0, 0, 0), False, 0
         # only a window of batches after the consumed prefix can be in flight
         win = 4 * (self.gk // gref + 1) * W + 64
-        while not done:
+
+        def launch(lo):
+            """Queue one graph of ticks, then the reduced rows [lo, lo + win) to
+            page-locked memory behind an event (stream-ordered, host not blocked)."""
             if self._graph is None:
                 self._ticks(sigma, lane_base, id_limit, n_batches, counts)      # eager first round
                 g = torch.cuda.CUDAGraph()
@@ -246,24 +294,38 @@ class RecycleCampaign:
                 self._graph = g
             else:
                 self._graph.replay()
-            end = min(n_batches, scan + win)
-            red = counts[scan:end].clone()
+            hi = min(n_batches, lo + win)
+            red = counts[lo:hi].clone()
             sum_counts(red, group)
-            rows = red.cpu().numpy()
+            host = torch.empty(tuple(red.shape), dtype=torch.int64, pin_memory=True)
+            host.copy_(red, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            return lo, host, ev
+
+        tot, done, scan = (0, 0, 0), False, 0
+        cur = launch(0)
+        while True:
+            nxt = launch(scan)      # look-ahead round, queued before this one is read
+            lo, host, ev = cur
+            ev.synchronize()
+            rows = host.numpy()[scan - lo:]
             # consume the prefix of complete batches in order (harness.py:173-192)
             hi = 0
             while hi < rows.shape[0] and rows[hi, 0] == gref:
                 hi += 1
             tot, done, used = ordered_prefix(rows[:hi], stop, max_frames, tot)
             scan += used
-            if not done and scan >= n_batches:
-                done = True
+            if done or scan >= n_batches:
+                break
+            cur = nxt
         torch.cuda.synchronize()
         return tot
 
 
 def run_block_simulation(layout: EdgeLayout, config: SimulationConfig, *,
-                         gamma_kernel: int | None = None, group=None, recycle: bool | None = None) -> list:
+                         gamma_kernel: int | None = None, group=None, recycle: bool | None = None,
+                         batches_per_launch: int | None = None) -> list:
     """Sweep the Eb/N0 points with the GPU block decoder (harness.py:157-204).
 
     early_stop campaigns on regular (J, 24) QC codes use lane recycling
@@ -277,7 +339,7 @@ def run_block_simulation(layout: EdgeLayout, config: SimulationConfig, *,
     info_bits = layout.n_vars - layout.n_checks
     gref = config.gamma
     max_units = max(1, -(-config.max_frames // (gref * W)))
-    units = _kernel_units(gref, gamma_kernel or 2048, max_units)
+    units = batches_per_launch or _kernel_units(gref, gamma_kernel or 2048, max_units)
     eng = BlockCampaign(layout, gref, units, config.iterations, config.early_stop, config.seed)
     results = []
     for pi, db in enumerate(config.points()):
@@ -285,16 +347,9 @@ def run_block_simulation(layout: EdgeLayout, config: SimulationConfig, *,
         lane_base = pi << 32
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        tot, done, rnd = (0, 0, 0), False, 0
-        while not done:
-            b0 = (rnd * W + rank) * units
-            eng.step(lane_base + b0 * gref, sigma)
-            allc = torch.zeros((W * units, 3), dtype=torch.int64, device=eng.counts.device)
-            allc[rank * units:(rank + 1) * units] = eng.counts
-            sum_counts(allc, g)
-            tot, done, _ = ordered_prefix(allc.cpu().numpy(), config.stop_block_errors,
-                                          config.max_frames, tot)
-            rnd += 1
+        tot = _run_rounds(lambda rnd: eng.step(lane_base + ((rnd * W + rank) * units) * gref, sigma),
+                          lambda: eng.counts, units, gref, rank, W, g, config.stop_block_errors,
+                          config.max_frames)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         frames, be, fe = tot
@@ -338,15 +393,16 @@ class StreamCampaign:
                  pushes: int, seed: int, graph: bool = True):
         torch = require_cuda()
         self.code, self.gref, self.S, self.I, self.pushes = code, gamma_ref, segments, processors, pushes
-        self.gk = gamma_ref * segments
+        self.gk = gamma_ref * segments          # counted lanes
+        self.gp = pad32(self.gk)                 # lanes the kernels run
         self.window = processors * (code.ms + 1)
         self.k0, self.k1 = seed_words(seed)
         self.plan = code.plan()
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.msg = torch.zeros((processors * code.edge_count, self.gk), dtype=torch.float32, device=dev)
-        self.ring = torch.zeros((self.window, code.c, self.gk), dtype=torch.float32, device=dev)
-        self.mu = torch.zeros((code.c, self.gk), dtype=torch.float32, device=dev)
-        self.cnt = torch.zeros((3, self.gk), dtype=torch.int32, device=dev)
+        self.msg = torch.zeros((processors * code.edge_count, self.gp), dtype=torch.float32, device=dev)
+        self.ring = torch.zeros((self.window, code.c, self.gp), dtype=torch.float32, device=dev)
+        self.mu = torch.zeros((code.c, self.gp), dtype=torch.float32, device=dev)
+        self.cnt = torch.zeros((3, self.gp), dtype=torch.int32, device=dev)
         self.lane0 = torch.zeros(1, dtype=torch.int64, device=dev)
         self.sigma = None
         self._graph = None
@@ -357,10 +413,10 @@ class StreamCampaign:
         self.cnt.zero_()
         for t in range(self.pushes):
             _lib.call("cc_channel", self.plan.handle, self.k0, self.k1, 0, self.lane0.data_ptr(), t, None,
-                      self.gk, float(self.sigma), self.mu.data_ptr(), s)
-            _lib.call("cc_slot", self.plan.handle, self.I, self.gk, t, None, self.msg.data_ptr(),
+                      self.gp, float(self.sigma), self.mu.data_ptr(), s)
+            _lib.call("cc_slot", self.plan.handle, self.I, self.gp, t, None, self.msg.data_ptr(),
                       self.ring.data_ptr(), self.mu.data_ptr(), None, self.cnt.data_ptr(), s)
-        _lib.call("cc_fold", self.cnt.data_ptr(), self.gk, s)
+        _lib.call("cc_fold", self.cnt.data_ptr(), self.gp, s)
 
     def kernel_launches_per_step(self) -> int:
         return self.pushes * 4 + 1      # channel, entry(+fold), check, variable; final fold
@@ -386,7 +442,7 @@ class StreamCampaign:
         """(S, 3) int64 (frames, bit_errors, frame_errors) per segment (device)."""
         import torch
         emitted = max(0, self.pushes - self.window + 1)
-        c = self.cnt.view(3, self.S, self.gref).to(torch.int64).sum(dim=2)
+        c = self.cnt[:, : self.gk].reshape(3, self.S, self.gref).to(torch.int64).sum(dim=2)
         out = torch.empty((self.S, 3), dtype=torch.int64, device=self.cnt.device)
         out[:, 0] = emitted * self.gref
         out[:, 1] = c[1]
@@ -395,7 +451,8 @@ class StreamCampaign:
 
 
 def run_stream_simulation(code: LdpcccCode, config: SimulationConfig, *,
-                          gamma_kernel: int | None = None, group=None) -> list:
+                          gamma_kernel: int | None = None, group=None,
+                          batches_per_launch: int | None = None) -> list:
     """Sweep the Eb/N0 points with the GPU pipelined stream decoder (harness.py:236-286)."""
     torch = require_cuda()
     rank, W, g = world() if group is None else (torch.distributed.get_rank(group),
@@ -407,7 +464,7 @@ def run_stream_simulation(code: LdpcccCode, config: SimulationConfig, *,
     gref = config.gamma
     per_seg = counted * gref
     max_units = max(1, -(-config.max_frames // (per_seg * W)))
-    units = _kernel_units(gref, gamma_kernel or 256, max_units)
+    units = batches_per_launch or _kernel_units(gref, gamma_kernel or 256, max_units)
     eng = StreamCampaign(code, gref, units, config.processors, pushes, config.seed)
     results = []
     for pi, db in enumerate(config.points()):
@@ -415,16 +472,9 @@ def run_stream_simulation(code: LdpcccCode, config: SimulationConfig, *,
         lane_base = pi << 32
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        tot, done, rnd = (0, 0, 0), False, 0
-        while not done:
-            s0 = (rnd * W + rank) * units
-            eng.step(lane_base + s0 * gref, sigma)
-            allc = torch.zeros((W * units, 3), dtype=torch.int64, device=eng.cnt.device)
-            allc[rank * units:(rank + 1) * units] = eng.segment_counts()
-            sum_counts(allc, g)
-            tot, done, _ = ordered_prefix(allc.cpu().numpy(), config.stop_block_errors,
-                                          config.max_frames, tot)
-            rnd += 1
+        tot = _run_rounds(lambda rnd: eng.step(lane_base + ((rnd * W + rank) * units) * gref, sigma),
+                          eng.segment_counts, units, per_seg, rank, W, g, config.stop_block_errors,
+                          config.max_frames)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         frames, be, fe = tot
@@ -440,10 +490,16 @@ def run_stream_simulation(code: LdpcccCode, config: SimulationConfig, *,
 
 def bench_throughput(layout: EdgeLayout | None, config: SimulationConfig,
                      code: LdpcccCode | None = None, frames: int = 256) -> list:
-    """Decoded-frames/s records for gamma in {1, config.gamma} (harness.py:294-331).
+    """Decoded-frames/s records for gamma in {1, config.gamma} x workers in
+    {1, cpu_count} (harness.py:294-331), same keys as the reference.
 
-    `workers` is recorded as in the reference; on the GPU it does not change
-    the execution (one process drives the device)."""
+    The reference's `workers` are processes that each decode one gamma-lane
+    batch at a time, so `workers` batches are in flight at once.  On the GPU
+    the same concurrency is one kernel launch over `workers` reference batches
+    side by side (gamma_kernel = workers x gamma lanes, padded to a multiple of
+    32; padding lanes are not counted): workers = 1 decodes one batch per
+    launch, workers = cores decodes cores batches per launch.  Each record
+    adds `batches_per_launch` and `lanes_per_launch` to say so."""
     cores = multiprocessing.cpu_count()
     records = []
     db = config.points()[0]
@@ -452,11 +508,15 @@ def bench_throughput(layout: EdgeLayout | None, config: SimulationConfig,
             cfg = dataclasses.replace(config, gamma=gamma, workers=workers, stop_block_errors=2**62,
                                       max_frames=frames, ebn0_db=db)
             if code is not None:
-                res = run_stream_simulation(code, cfg)[0]
+                per_unit = (config.stream_segment_frames or
+                            max(2 * (config.processors * (code.ms + 1) - 1), 64)) * gamma
+                units = min(workers, max(1, -(-frames // per_unit)))
+                res = run_stream_simulation(code, cfg, batches_per_launch=units)[0]
                 meta = dict(mode="stream", n=code.c, m=code.cb, edge_count=code.edge_count,
                             iters_or_I=config.processors)
             else:
-                res = run_block_simulation(layout, cfg)[0]
+                units = min(workers, max(1, -(-frames // gamma)))
+                res = run_block_simulation(layout, cfg, batches_per_launch=units, recycle=False)[0]
                 meta = dict(mode="block", n=layout.n_vars, m=layout.n_checks,
                             edge_count=layout.edge_count, iters_or_I=config.iterations)
             records.append(dict(
@@ -465,5 +525,6 @@ def bench_throughput(layout: EdgeLayout | None, config: SimulationConfig,
                 frames_per_sec=round(res.frames_per_sec, 3),
                 info_bits_per_sec=round(res.info_bits_per_sec, 1),
                 per_frame_ms=round(1000 * res.seconds / res.frames, 4) if res.frames else None,
+                batches_per_launch=units, lanes_per_launch=pad32(units * gamma),
                 **meta))
     return records

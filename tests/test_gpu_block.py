@@ -472,3 +472,112 @@ def test_compact_schedule_decode_is_bit_identical(gpu, tmp_path):
             outs.append(np.load(f))
         for o in outs[1:]:
             assert np.array_equal(outs[0], o), gamma
+
+
+def rel_err(got, ref, atol=1e-12):
+    """|delta| / (|ref| + atol): the north star's relative measure (atol only
+    guards exact zeros of the reference; fp32 cannot represent below ~1e-38)."""
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    return np.abs(got - ref) / (np.abs(ref) + atol)
+
+
+def test_single_step_relative_tolerance(gpu):
+    """One public check + variable update on identical fp32-representable inputs
+    against the float64 reference (bp.py:134-188), in RELATIVE terms:
+    * check update: |d alpha| <= 1e-4 |alpha| (atol 1e-12 only guards exact zeros);
+    * variable update and posterior: |d| <= 1e-4 |ref| + 2^-20 (|mu| + sum |alpha|)
+      -- the second term is a few ulp of fp32 rounding of the running total
+      itself (bp.py:179-182: total - alpha and the total cancel when the terms
+      have mixed signs), which no fp32 implementation can avoid."""
+    q = gpu
+    rng = np.random.default_rng(5)
+    w_c = w_v = w_p = 0.0
+    for d in (2, 3, 4, 6, 8, 16, 24, 32):
+        n = d + 5
+        rows = [sorted(rng.choice(n, size=d, replace=False)) for _ in range(6)]
+        lay = q.build_edge_layout(q.SparseParityCheck(n, rows))
+        olay = oqc.layout_from_rows(n, rows)
+        mu = rng.normal(0, 1, size=(n, 64)) * rng.choice([0.01, 0.1, 1, 5, 20, 60], size=(n, 1))
+        mu = np.clip(mu, -50, 50).astype(np.float32).astype(np.float64)
+        b = q.MessageBatch(lay, mu)
+        q.check_node_update(b, lay)
+        ob = obp.init_buffer(olay, mu)
+        obp.check_update(ob, olay)
+        w_c = max(w_c, rel_err(b.packages, ob[:-1]).max())
+        ob[:-1] = b.packages.astype(np.float32).astype(np.float64)
+        mag = np.abs(mu) + np.abs(ob[olay.var_pad]).sum(axis=1)          # |mu| + sum |alpha| per (n, lane)
+        post = q.variable_node_update(b, lay)
+        opost = obp.var_update(ob, mu, olay)
+        w_p = max(w_p, (np.abs(post - opost) / (TOL * np.abs(opost) + 2.0 ** -20 * mag)).max())
+        scale = np.zeros_like(ob[:-1])
+        for k in range(olay.var_pad.shape[1]):
+            e = olay.var_pad[:, k]
+            ok = e < olay.edge_count
+            scale[e[ok]] = mag[ok]
+        w_v = max(w_v, (np.abs(b.packages - ob[:-1]) / (TOL * np.abs(ob[:-1]) + 2.0 ** -20 * scale)).max())
+    print(f"check: max relative error {w_c:.3e} (<= 1e-4); variable / posterior: max of "
+          f"|d| / (1e-4 |ref| + 2^-20 magnitude) = {w_v:.3f} / {w_p:.3f} (<= 1)")
+    assert w_c <= TOL and w_p <= 1.0 and w_v <= 1.0
+
+
+@pytest.mark.parametrize("shape", ["irregular", "qc"])
+def test_masked_single_steps(gpu, shape):
+    """check_node_update / variable_node_update with an `active` lane mask
+    (bp.py:154-157, 183-187): frozen lanes keep their packages bit for bit,
+    active lanes update, and the posteriors of EVERY lane -- frozen ones
+    included -- are clip(mu + sum alpha)."""
+    q = gpu
+    rng = np.random.default_rng(11)
+    if shape == "qc":
+        exp = q.multiplicative_shifts(3, 6, 11)
+        lay = q.build_edge_layout(q.expand_qc(exp))
+        olay = oqc.qc_layout(exp.shifts, exp.p)
+        n = lay.n_vars
+    else:
+        n = 40
+        rows = [sorted(rng.choice(n, size=int(rng.integers(2, 9)), replace=False)) for _ in range(22)]
+        lay = q.build_edge_layout(q.SparseParityCheck(n, rows))
+        olay = oqc.layout_from_rows(n, rows)
+    G = 96
+    mu = np.clip(rng.normal(1.5, 2.5, size=(n, G)), -50, 50).astype(np.float32).astype(np.float64)
+    b = q.MessageBatch(lay, mu)
+    ob = obp.init_buffer(olay, mu)
+    for step in range(3):
+        active = rng.random(G) < 0.6
+        active[:2] = [True, False]
+        before = b.packages.copy()
+        q.check_node_update(b, lay, active)
+        obp.check_update(ob, olay, active)
+        close(b.packages, ob[:-1])
+        assert np.array_equal(b.packages[:, ~active], before[:, ~active])
+        ob[:-1] = b.packages.astype(np.float32).astype(np.float64)     # identical inputs to the next step
+        before = b.packages.copy()
+        post = q.variable_node_update(b, lay, active)
+        opost = obp.var_update(ob, mu, olay, active)
+        close(post, opost)                                         # all lanes, frozen too
+        close(b.packages, ob[:-1])
+        assert np.array_equal(b.packages[:, ~active], before[:, ~active])
+        ob[:-1] = b.packages.astype(np.float32).astype(np.float64)
+
+
+def test_packages_view_semantics(gpu):
+    """MessageBatch.packages behaves like the reference's writable view
+    (bp.py:82-84): one host mirror, refreshed in place by updates, caller
+    writes honoured by the next update."""
+    q = gpu
+    lay = toy(q)
+    mu = np.random.default_rng(2).normal(2, 2, size=(lay.n_vars, 32)).astype(np.float32).astype(np.float64)
+    b = q.MessageBatch(lay, mu)
+    pk = b.packages
+    assert b.packages is pk                       # O(1) after the first access
+    assert np.array_equal(pk, mu[lay.edge_var])
+    q.check_node_update(b, lay)
+    olay = oqc.qc_layout(q.multiplicative_shifts(2, 4, 8).shifts, 8)
+    ob = obp.init_buffer(olay, mu)
+    obp.check_update(ob, olay)
+    close(pk, ob[:-1])                            # the held array saw the update
+    pk[:, 5] = 0.75                               # write through the view
+    ob[:-1] = pk
+    q.check_node_update(b, lay)
+    obp.check_update(ob, olay)
+    close(b.packages, ob[:-1])

@@ -8,7 +8,7 @@ import socket
 import pytest
 import torch
 import torch.multiprocessing as mp
-from conftest import GOLDEN
+from conftest import GOLDEN, REPO
 
 pytestmark = pytest.mark.gpu
 
@@ -48,7 +48,7 @@ def test_two_ranks_share_counters():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     camp = json.load(open(os.path.join(GOLDEN, "campaigns.json")))
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()     # never fork after CUDA init
     out = mgr.dict()
     mp.spawn(_rank, args=(2, _port(), out), nprocs=2, join=True)
     assert out[0] == out[1]
@@ -58,3 +58,33 @@ def test_two_ranks_share_counters():
     want = campaign.block_point(oqc.qc_layout(oqc.array_code_shifts(4, 24, 29), 29), 2.6, 0, iters=20,
                                 gamma=32, seed=2, stop=9, max_frames=4000, early_stop=True)
     assert tuple(out[0][2][0][5:8]) == want
+
+
+def _bench(args, env_extra=None):
+    import subprocess
+    import sys
+    repo = REPO
+    env = dict(os.environ, **(env_extra or {}))
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), *args], capture_output=True, text=True,
+                       env=env, timeout=900, cwd=repo)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    return json.loads(line), r.stderr
+
+
+def test_bench_gpus_2_entry_path_matches_one_rank():
+    """`python bench.py --gpus 2` (no torchrun env) launches 2 ranks itself; with
+    gloo both share the one GPU.  Rank r of step s decodes lanes (s*W + r)*gamma,
+    so 2 ranks x 256 lanes cover the lanes of 1 rank x 512: the summed counters
+    of the last step must be identical."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    common = ["--steps", "3", "--warmup", "3", "--no-e2e", "--stream-gamma", "0", "--no-cpu",
+              "--sustain-s", "0"]
+    two, err = _bench(["--gpus", "2", "--gamma", "256", *common], {"QCB_DIST_BACKEND": "gloo"})
+    one, _ = _bench(["--gpus", "1", "--gamma", "512", *common])
+    assert two["n_gpus"] == 2 and one["n_gpus"] == 1
+    assert two["communicator"]["world_size"] == 2 and two["communicator"]["ranks_summed"] == 2
+    assert "launching 2 ranks" in err
+    assert two["counts_last_step"] == one["counts_last_step"]
+    assert two["counts_last_step"]["frames"] == 512

@@ -8,6 +8,8 @@ import numpy as np
 import pytest
 from conftest import GOLDEN
 
+from oracle import channel as och
+
 pytestmark = pytest.mark.gpu
 CAMP = json.load(open(os.path.join(GOLDEN, "campaigns.json")))
 
@@ -187,3 +189,53 @@ def test_stream_counts_match_manual_replay(gpu):
                 frame_errors += int(fr.hard_bits.any(axis=1).sum())
     assert (res.frames, res.bit_errors, res.frame_errors) == (frames, bit_errors, frame_errors)
     assert res.iters_or_i == 2
+
+
+BENCH = json.load(open(os.path.join(GOLDEN, "campaigns_bench.json")))
+
+
+def _n18360(q, codes_npz):
+    return q.ExponentMatrix(codes_npz["n18360_shifts"], int(codes_npz["n18360_p"]))
+
+
+def test_bench_config_block_campaign(gpu, codes_npz):
+    """bench.py's block configuration (n18360, 30 it, gamma_kernel 1024 lanes per
+    launch = 32 reference batches) reproduces the reference harness's counts
+    (tests/golden/make_golden_bench.py: 1024 frames at 3.0 dB)."""
+    q = gpu
+    lay = q.build_edge_layout(q.expand_qc(_n18360(q, codes_npz)))
+    cfg = q.SimulationConfig("n18360", [3.0], iterations=30, gamma=32, stop_block_errors=2**62,
+                             max_frames=1024, seed=0)
+    res = q.run_block_simulation(lay, cfg, batches_per_launch=32)        # 1024 lanes per launch
+    assert [r.row()[:10] for r in res] == BENCH["n18360_block_3.0dB_30it_1024"]
+
+
+def test_decode_batch_gamma_1024_replicated_golden(gpu, codes_npz):
+    """decode_batch at gamma 1024 (the host pipeline's 512-lane chunks, fused
+    compact-schedule kernels) on the 32 golden n18360 lanes replicated 32 times:
+    every copy's bits and syndrome flag equal the reference's."""
+    q = gpu
+    from conftest import golden
+    g = golden("block_n18360.npz")
+    lay = q.build_edge_layout(q.expand_qc(_n18360(q, codes_npz)))
+    sigma = float(g["sigma"])
+    y = och.received(0, sigma, 0, 32, lay.n_vars)
+    yy = np.ascontiguousarray(np.tile(y, (32, 1)))
+    r = q.decode_batch(lay, yy, sigma, 30)
+    bits = np.packbits(r.hard_bits, axis=1).reshape(32, 32, -1)
+    assert all(np.array_equal(bits[k], g["bits"]) for k in range(32))
+    assert np.array_equal(r.syndrome_ok, np.tile(g["ok"], 32))
+    assert np.array_equal(r.hard_bits.sum(axis=1), np.tile(g["bit_errors"], 32))
+
+
+@pytest.mark.slow
+def test_bench_config_stream_campaign(gpu, codes_npz):
+    """bench.py's LDPCCC configuration (18360' = the n18360 grid unwrapped,
+    I = 20, gamma_kernel 512 = 16 reference segments side by side) reproduces the
+    reference harness's counts for its first segment (5056 frames at 3.1 dB)."""
+    q = gpu
+    code = q.unwrap_qc(_n18360(q, codes_npz))
+    cfg = q.SimulationConfig("n18360p", [3.1], processors=20, gamma=32, stop_block_errors=2**62,
+                             max_frames=5056, seed=0)
+    res = q.run_stream_simulation(code, cfg, batches_per_launch=16)      # 512 lanes per launch
+    assert [r.row()[:10] for r in res] == BENCH["n18360p_stream_3.1dB_I20_5056"]

@@ -141,3 +141,33 @@ def test_campaign_worker_invariance():
     b = campaign.block_point(lay, 2.0, 0, iters=8, gamma=8, seed=5, stop=15, max_frames=2000,
                              workers=2)
     assert a == b
+
+
+def test_reference_oracles_restatement_matches_reference():
+    """oracle/reference.py (exact_posterior_llr, reference_window_decoder) equals the
+    reference's own qcldpc.reference (reference.py:25-182) bit for bit."""
+    import pytest
+    from oracle import build_ref
+    if not build_ref.available():
+        pytest.skip("oracle/_ref not built")
+    import importlib
+    import sys
+    sys.path.insert(0, build_ref.site_dir())
+    try:
+        ref = importlib.import_module("qcldpc.reference")
+        qcl = importlib.import_module("qcldpc")
+    finally:
+        sys.path.remove(build_ref.site_dir())
+    from oracle import reference as ours
+    rng = np.random.default_rng(3)
+    h = qcl.SparseParityCheck(8, [[0, 1, 2], [2, 3, 4], [4, 5, 6, 7], [0, 7], [1, 5]])
+    for _ in range(4):
+        mu = rng.normal(0, 1.5, 8)
+        np.testing.assert_allclose(ours.exact_posterior_llr(h, mu), ref.exact_posterior_llr(h, mu),
+                                   rtol=0, atol=1e-12)
+    code = qcl.unwrap_qc(qcl.multiplicative_shifts(4, 24, 8))
+    llrs = [qcl.channel_llrs(rng.normal(1, 0.8, (1, code.c)), 0.8)[0] for _ in range(14)]
+    b0, p0 = ref.reference_window_decoder(code, 2, llrs)
+    b1, p1 = ours.reference_window_decoder(code, 2, llrs)
+    assert all(np.array_equal(x, y) for x, y in zip(b0, b1))
+    assert all(np.array_equal(x, y) for x, y in zip(p0, p1))

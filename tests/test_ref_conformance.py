@@ -1,0 +1,68 @@
+"""The reference's OWN test suite against the drop-in.
+
+oracle/build_ref.py installs the unmodified reference tests into git-ignored
+oracle/_ref/ref_tests; tests/ref_suite_shim.py aliases `qcldpc` to
+paper_1204_0334_b200.  The suite runs twice, on the float32 production path
+and on the float64 conformance build (set_precision), and every test must pass
+except the ones listed in EXPECTED with the reason it cannot (DESIGN.md
+section "Reference-suite conformance").  The per-test outcome lists are
+written to gpurun_out/ref_conformance.json (committed copy under profiles/).
+"""
+import json
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUITE = os.path.join(REPO, "oracle", "_ref", "ref_tests")
+
+# test id -> reason it is allowed to fail, per precision
+EXPECTED = {
+    "float32": {},
+    "float64": {},
+}
+
+
+def run_suite(precision: str, tmp):
+    xml = os.path.join(tmp, f"ref_{precision}.xml")
+    env = dict(os.environ, QCLDPC_B200_PRECISION=precision,
+               PYTHONPATH=os.pathsep.join([os.path.join(REPO, "tests"), REPO]))
+    r = subprocess.run([sys.executable, "-m", "pytest", SUITE, "-p", "ref_suite_shim", "-q",
+                        "-p", "no:cacheprovider", "--continue-on-collection-errors", f"--junitxml={xml}", "-o", "junit_family=xunit1"],
+                       cwd=tmp, env=env, capture_output=True, text=True, timeout=3000)
+    out = {}
+    for case in ET.parse(xml).getroot().iter("testcase"):
+        tid = f"{case.get('classname', '').split('.')[-1]}::{case.get('name')}"
+        kind = "passed"
+        for tag in ("failure", "error", "skipped"):
+            el = case.find(tag)
+            if el is not None:
+                kind = tag
+                msg = (el.get("message") or "").splitlines()
+                out[tid] = {"outcome": kind, "message": msg[0][:300] if msg else ""}
+                break
+        else:
+            out[tid] = {"outcome": kind}
+    return out, r.stdout[-3000:]
+
+
+def test_reference_suite_against_drop_in(tmp_path):
+    if not os.path.isdir(SUITE):
+        pytest.skip("oracle/_ref not built (python -m oracle.build_ref in the build container)")
+    report, bad = {}, []
+    for prec in ("float32", "float64"):
+        res, tail = run_suite(prec, str(tmp_path))
+        npass = sum(v["outcome"] == "passed" for v in res.values())
+        report[prec] = {"passed": npass, "total": len(res), "tests": res, "tail": tail}
+        for tid, v in res.items():
+            if v["outcome"] != "passed" and tid not in EXPECTED[prec]:
+                bad.append((prec, tid, v.get("message", "")))
+    os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(REPO, "gpurun_out", "ref_conformance.json"), "w") as fh:
+        json.dump({"expected_failures": EXPECTED, "results": report}, fh, indent=1)
+    assert not bad, bad
