@@ -383,48 +383,29 @@ int env_int(const char* name, int dflt) {
 }
 
 int agg_mode() {
-  static int v = env_int("QCB_AGG", 1);   // 0 = two-pass schedule (A/B experiments)
+  // 0 = the two-pass reference schedule inside qc_decode: the A/B oracle of the
+  // bit-identity tests (tests/test_gpu_block.py), not a tuning knob
+  static int v = env_int("QCB_AGG", 1);
   return v;
 }
-int agg_lanes() {
-  static int v = env_int("QCB_AGG_LG", 128);
-  return v;
-}
-int agg_tile() {
-  static int v = env_int("QCB_AGG_TILE", 0);   // >0: lanes decoded together (measured: no gain, the strided tile rows cost more)
-  return v;
-}
-int agg_reverse() {
-  static int v = env_int("QCB_AGG_REV", 1);
-  return v;
-}
-int agg_fused_mode() {
-  static int v = env_int("QCB_AGG_FUSED", 1);    // 0 = unfused compact passes
-  return v;
-}
-int agg_vv() {
-  static int v = env_int("QCB_AGG_VV", 4);       // lanes per thread of the variable job (4 or 2)
-  return v == 2 ? 2 : 4;
-}
-int agg_items() {
-  static int v = env_int("QCB_AGG_ITEMS", 2);    // rows per variable thread (2: L2 prefetch of the next; +1.5%)
-  return v == 1 ? 1 : 2;
-}
-int agg_fused_vc() {
-  static int v = env_int("QCB_AGG_FVC", 4);      // lanes per thread of the fused check job (4: +2.4% at 128-thread CTAs)
-  return v == 2 ? 2 : 4;
-}
+
+// Measured optimum of the compact schedule on B200 (profiles/r01/kbench_compact_*.jsonl):
+constexpr int AGG_LANE_GROUP = 128;   // lanes per lane group (check-record L2 working set)
+constexpr int AGG_REVERSE = 1;        // variable job visits lane groups last-to-first
+constexpr int AGG_VV = 4;             // lanes per thread of the standalone variable job
+constexpr int AGG_ITEMS = 2;          // rows per variable thread (L2 prefetch of the second, +1.5%)
+constexpr int AGG_FVC = 4;            // lanes per thread of the fused check job (+2.4% over 2)
 
 bool dc_supported(int dc) { return dc == 4 || dc == 6 || dc == 8 || dc == 12 || dc == 16 || dc == 24 || dc == 32; }
 bool dv_supported(int dv) { return dv >= 2 && dv <= 4; }
 
 int pick_vec(int gamma) { return gamma % 128 == 0 ? 4 : (gamma % 64 == 0 ? 2 : 1); }
-int pick_vec_var(int gamma) { return std::min(pick_vec(gamma), agg_vv()); }
+int pick_vec_var(int gamma) { return std::min(pick_vec(gamma), AGG_VV); }
 
 // log2 of the lane vectors per group: the largest power of two <= LG/VEC that
 // divides GV = gamma/VEC (GV is a multiple of 32 for every vec pick_vec returns)
 int pick_lg_gw(int gamma, int vec) {
-  int GV = gamma / vec, target = std::max(32, agg_lanes() / vec), lg = 5;
+  int GV = gamma / vec, target = std::max(32, AGG_LANE_GROUP / vec), lg = 5;
   while ((2 << lg) <= target && GV % (2 << lg) == 0) ++lg;
   return lg;
 }
@@ -477,13 +458,8 @@ void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) 
 
 template <int DV, int VEC>
 void launch_var_v(AggArgs a, int flags, const QcGrid& g, cudaStream_t s) {
-
-  if (agg_items() >= 2) {      // standalone variable pass: at most 2 rows per thread
-    a.rows_eff = (a.rows + 1) / 2;
-    launch_var_i<DV, VEC, 2>(a, flags, g, s);
-  } else {
-    launch_var_i<DV, VEC, 1>(a, flags, g, s);
-  }
+  a.rows_eff = (a.rows + AGG_ITEMS - 1) / AGG_ITEMS;      // standalone variable pass: AGG_ITEMS rows per thread
+  launch_var_i<DV, VEC, AGG_ITEMS>(a, flags, g, s);
 }
 
 template <int DV>
@@ -501,8 +477,7 @@ void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaSt
 
 template <int DC, int DV, int VC, bool FROM_MU, int FLAGS>
 void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t s) {
-  if (agg_items() >= 2) launch_k(agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 2>, grid, s, f, g);
-  else launch_k(agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, 1>, grid, s, f, g);
+  launch_k(agg_fused_kernel<DC, DV, VC, AGG_FUSED_VV, FROM_MU, FLAGS, AGG_ITEMS>, grid, s, f, g);
 }
 
 template <int DC, int DV, int VC>
@@ -523,10 +498,8 @@ int launch_fused_v(const FusedArgs& f, dim3 grid, bool from_mu, int flags, const
 }
 
 template <int DC, int DV>
-int launch_fused_dc(const FusedArgs& f, dim3 grid, int vc, bool from_mu, int flags, const QcGrid& g,
-                    cudaStream_t s) {
-  return vc == 4 ? launch_fused_v<DC, DV, 4>(f, grid, from_mu, flags, g, s)
-                 : launch_fused_v<DC, DV, 2>(f, grid, from_mu, flags, g, s);
+int launch_fused_dc(const FusedArgs& f, dim3 grid, bool from_mu, int flags, const QcGrid& g, cudaStream_t s) {
+  return launch_fused_v<DC, DV, AGG_FVC>(f, grid, from_mu, flags, g, s);
 }
 
 unsigned long long magic40(unsigned d) { return ((1ull << 40) + d - 1) / d; }
@@ -534,7 +507,7 @@ unsigned long long magic40(unsigned d) { return ((1ull << 40) + d - 1) / d; }
 }  // namespace
 
 bool agg_fused_eligible(const qc_plan* p, int gamma) {
-  return agg_fused_mode() != 0 && agg_eligible(p) && gamma % 256 == 0 &&
+  return agg_eligible(p) && gamma % 256 == 0 &&
          ((p->L == 24 && p->J == 4) || (p->L == 4 && p->J == 2));
 }
 
@@ -552,11 +525,10 @@ int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, 
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
                         const uint32_t* active, const int32_t* v_done, const int32_t* c_done, cudaStream_t s) {
-  const int vc = agg_fused_vc();
   FusedArgs f;
-  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, agg_reverse());
-  f.v.rows_eff = (f.v.rows + agg_items() - 1) / agg_items();
-  f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, vc, 0);
+  f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, AGG_REVERSE);
+  f.v.rows_eff = (f.v.rows + AGG_ITEMS - 1) / AGG_ITEMS;
+  f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, AGG_FVC, 0);
   f.v.active = f.c.active = active;
   f.v.done = v_done;
   f.c.done = c_done;
@@ -569,8 +541,8 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
   f.R = (f.nbv + nbc - 1) / nbc;
   const dim3 grid(f.R + 1, nbc, 1);
   const QcGrid g = make_grid(p);
-  int rc = (p->L == 24) ? launch_fused_dc<24, 4>(f, grid, vc, from_mu, flags, g, s)
-                        : launch_fused_dc<4, 2>(f, grid, vc, from_mu, flags, g, s);
+  int rc = (p->L == 24) ? launch_fused_dc<24, 4>(f, grid, from_mu, flags, g, s)
+                        : launch_fused_dc<4, 2>(f, grid, from_mu, flags, g, s);
   if (rc) return rc;
   return check_launch("agg_fused");
 }
@@ -627,7 +599,7 @@ int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flag
                      const int32_t* done) {
   const int vec = pick_vec_var(lanes);
   AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
-                        agg_reverse());
+                        AGG_REVERSE);
   a.active = active;
   a.done = done;
   const QcGrid g = make_grid(p);
@@ -648,21 +620,9 @@ int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flag
 int run_agg_tile(const qc_plan* p, int gamma, int lane0, int lanes, int iters, float* msgs, const float* mu,
                  float* agg, float* post, uint32_t* hb, cudaStream_t s);
 
-// Lanes are decoded in tiles of agg_tile() lanes, one complete flooding loop
-// per tile: a tile's check records (3 M x tile words, 37 MB for n18360 at 1024
-// lanes) stay L2-resident between the passes.
 int run_agg_decode(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
                    uint32_t* hb, cudaStream_t s) {
-  const int T = agg_tile_lanes(p, gamma);
-  for (int l0 = 0; l0 < gamma; l0 += T)
-    if (int rc = run_agg_tile(p, gamma, l0, std::min(T, gamma - l0), iters, msgs, mu, agg, post, hb, s)) return rc;
-  return 0;
-}
-
-int agg_tile_lanes(const qc_plan* p, int gamma) {
-  const int t = agg_tile();
-  if (t <= 0 || t >= gamma || t % 256 || gamma % t || !agg_fused_eligible(p, gamma)) return gamma;
-  return t;
+  return run_agg_tile(p, gamma, 0, gamma, iters, msgs, mu, agg, post, hb, s);
 }
 
 int run_agg_tile(const qc_plan* p, int gamma, int lane0, int lanes, int iters, float* msgs, const float* mu,
@@ -740,8 +700,7 @@ int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const
 }
 
 int agg_decode_launches(const qc_plan* p, int gamma, int iters) {
-  const int T = agg_tile_lanes(p, gamma);
-  return (gamma / T) * (agg_fused_eligible(p, T) ? 2 * iters + 1 : 2 * iters);
+  return agg_fused_eligible(p, gamma) ? 2 * iters + 1 : 2 * iters;
 }
 
 }  // namespace qcb

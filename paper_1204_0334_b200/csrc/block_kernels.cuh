@@ -272,17 +272,9 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
   if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, valid);
 }
 
-// lanes per thread: float4 packages at large gamma, narrower when gamma is
-// small (more threads) or the check degree is large (registers)
-int vec_override();   // QCB_VEC env (tuning experiments); 0 = automatic
-
 // check pass: 2 lanes per thread (float2) -- measured best on B200 at d_c = 24
 // (4 lanes: 171 registers, 8 warps/SM; 1 lane: LSU-issue bound)
-inline int pick_vec_cnu(int gamma, int dc) {
-  int o = vec_override();
-  if (o == 1 || (o == 2 && gamma % 64 == 0) || (o == 4 && gamma % 128 == 0 && dc <= 24)) return o;
-  return gamma % 64 == 0 ? 2 : 1;
-}
+inline int pick_vec_cnu(int gamma, int) { return gamma % 64 == 0 ? 2 : 1; }
 // variable pass: float4 packages
 inline int pick_vec_vnu(int gamma) {
   if (gamma % 128 == 0) return 4;
@@ -291,9 +283,6 @@ inline int pick_vec_vnu(int gamma) {
 
 QcGrid make_grid(const qc_plan* p);
 
-// persistent cp.async-pipelined check pass (cnu_pipe.cu); 0 if not applicable
-int launch_cnu_phi_pipe(const qc_plan* p, const CnuArgs& a, cudaStream_t s);
-int cnu_pipe_mode();   // QCB_CNU_PIPE env: 1 = use the pipelined check pass
 
 // compact check-state schedule (agg.cu)
 constexpr int AGG_FIRST_FLAG = 1, AGG_LAST_FLAG = 2;
@@ -306,7 +295,6 @@ int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const fl
 int run_agg_decode(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
                    uint32_t* hb, cudaStream_t s);
 int agg_decode_launches(const qc_plan* p, int gamma, int iters);
-int agg_tile_lanes(const qc_plan* p, int gamma);
 bool agg_es_eligible(const qc_plan* p, int gamma);
 int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
                       uint32_t* hb, uint32_t* bad, uint32_t* active, int32_t* done, uint8_t* ok, int32_t* iters_run,

@@ -31,11 +31,7 @@ int launch_cnu_v(const qc_plan* p, const CnuArgs& a, int mode, cudaStream_t s) {
 
 template <int DC>
 int launch_cnu_dc(const qc_plan* p, const CnuArgs& a, int mode, cudaStream_t s) {
-  if constexpr (DC == 24) {
-    if (mode == CNU_PHI && cnu_pipe_mode() >= 1 && launch_cnu_phi_pipe(p, a, s)) return 0;
-  }
   switch (pick_vec_cnu(a.gamma, DC)) {
-    case 4: if constexpr (DC <= 24) return launch_cnu_v<DC, 4>(p, a, mode, s); else return -1;
     case 2: return launch_cnu_v<DC, 2>(p, a, mode, s);
     default: return launch_cnu_v<DC, 1>(p, a, mode, s);
   }

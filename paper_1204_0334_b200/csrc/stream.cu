@@ -88,7 +88,7 @@ __device__ __forceinline__ int pmod(int x, int m) {
 
 // Edges of variable v (block column bc, circulant column cc) of a frame with
 // phase ph in group base `grp`, in the reference's summation order
-// (d = 0..T-1 over LUT_v[ph][d], then block row br; convolutional.py:414-423).
+// (d = 0..T-1 over LUT_v[ph][d], then block row br; convolutional.py:136-151, 307-317).
 // QC: local id of (br, bc) in sub-block (R, ph) = (br*p + (cc - s) mod p)*sl + bc.
 // Shift lookups are warp-uniform (gamma/VEC >= 32: a warp is one variable) and
 // read straight from the __grid_constant__ parameter bank.

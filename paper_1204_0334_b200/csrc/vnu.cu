@@ -7,14 +7,6 @@
 
 namespace qcb {
 
-int vec_override() {
-  static int v = [] {
-    const char* e = std::getenv("QCB_VEC");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 QcGrid make_grid(const qc_plan* p) {
   QcGrid g;
   std::memset(&g, 0, sizeof(g));

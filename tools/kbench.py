@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Kernel micro-benchmark: per-pass CUDA-event times of the decode-loop kernels
 (check pass in phi form, variable pass in phi form) and whole-decode time, for
-a list of gamma values.  One JSON line per gamma.  QCB_VEC=1|2|4 overrides the
-lanes-per-thread choice (set it in the environment of this process).
+a list of gamma values.  One JSON line per gamma.  QCB_AGG=0 times the
+two-pass reference schedule instead of the compact one.
 
   python tools/kbench.py --gammas 256 1024 2048 --reps 20
 """
@@ -62,7 +62,7 @@ def main():
                                                               dec.mu.data_ptr(), agg_ptr, st))
             agg_ms["agg_var_ms"] = timeit(lambda: _lib.call("qc_agg_var", p, G, 0, dec.msgs.data_ptr(),
                                                             dec.mu.data_ptr(), agg_ptr, None, None, st))
-            if G % 256 == 0 and os.environ.get("QCB_AGG_FUSED", "1") != "0":
+            if G % 256 == 0:
                 H = G // 2
                 agg_ms["agg_fused_half_ms"] = timeit(lambda: _lib.call(
                     "qc_agg_fused", p, G, H, 0, 0, H, 0, dec.msgs.data_ptr(), dec.mu.data_ptr(), agg_ptr,
@@ -75,7 +75,7 @@ def main():
         cb, vb = 2 * E * G * 4, (2 * E + N) * G * 4
         alg = 4 * (30 * (4 * E + N) + (N + E)) * G
         print(json.dumps({
-            "gamma": G, "vec_env": os.environ.get("QCB_VEC", "auto"),
+            "gamma": G,
             "cnu_phi_ms": round(cnu_phi, 4), "cnu_phi_gbs": round(cb / cnu_phi / 1e6, 1),
             "cnu_from_mu_ms": round(cnu_mu, 4),
             "vnu_phi_ms": round(vnu_phi, 4), "vnu_phi_gbs": round(vb / vnu_phi / 1e6, 1),
@@ -83,8 +83,7 @@ def main():
             "decode_frac": round(alg / dec_ms / 1e6 / peak, 4),
             "mbit_s": round(G * (N - lay.n_checks) / dec_ms / 1e3, 1),
             **{k: round(v, 4) for k, v in agg_ms.items()},
-            "agg_env": os.environ.get("QCB_AGG", "1"), "agg_lg": os.environ.get("QCB_AGG_LG", "512"),
-            "fused": os.environ.get("QCB_AGG_FUSED", "1"), "fvc": os.environ.get("QCB_AGG_FVC", "2"), "vv": os.environ.get("QCB_AGG_VV", "4"),
+            "agg_env": os.environ.get("QCB_AGG", "1"),
             "early_stop": args.early_stop, "ebn0_db": args.ebn0, "mean_iterations": round(mean_it, 2)}), flush=True)
         del dec
         torch.cuda.empty_cache()
