@@ -399,8 +399,7 @@ def main():
     st = _lib.stream_handle()
     reps = 20
     H = gamma // 2
-    W32 = gamma // 32
-    agg_ptr = dec.work.data_ptr() + ((2 * W32 + 4 + 63) // 64 * 64) * 4    # records region (qc_decode_work_words)
+    agg_ptr = dec.work.data_ptr() + int(_lib.load().qc_decode_records_offset(gamma)) * 4   # records region
     fused = lambda: _lib.call("qc_agg_fused", dec.plan.handle, gamma, H, 0, 0, H, 0, dec.msgs.data_ptr(),
                               dec.mu.data_ptr(), agg_ptr, None, None, st)
     check = lambda: _lib.call("qc_agg_check", dec.plan.handle, gamma, 0, dec.msgs.data_ptr(), dec.mu.data_ptr(),

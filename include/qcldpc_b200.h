@@ -94,6 +94,9 @@ QC_API int qc_bit_errors(const qc_plan* plan, int gamma, const uint32_t* hb, int
  * ok (gamma) u8 out; iters_run (gamma) i32 out; lane_bits (gamma) i32 out
  * (may be NULL).  early_stop reproduces bp.py:242-256 (freeze on syndrome). */
 QC_API size_t qc_decode_work_words(const qc_plan* plan, int gamma);
+/* word offset of the compact check records inside that work buffer (for the
+ * qc_agg_* pass entry points used by benchmarks and tests). */
+QC_API size_t qc_decode_records_offset(int gamma);
 QC_API int qc_decode(const qc_plan* plan, int gamma, int iters, int early_stop, const float* mu,
               float* msgs, float* post, uint32_t* hb, uint32_t* work, uint8_t* ok,
               int32_t* iters_run, int32_t* lane_bits, void* stream);

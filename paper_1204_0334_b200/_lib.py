@@ -38,6 +38,7 @@ SIGNATURES = {
     "qc_hard_bits": (_i, [_p, _i, _p, _p, _p]),
     "qc_bit_errors": (_i, [_p, _i, _p, _p, _p]),
     "qc_decode_work_words": (C.c_size_t, [_p, _i]),
+    "qc_decode_records_offset": (C.c_size_t, [_i]),
     "qc_decode": (_i, [_p, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "qc_agg_check": (_i, [_p, _i, _i, _p, _p, _p, _p]),
     "qc_agg_var": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p]),

@@ -23,6 +23,7 @@
 // check records a variable pass gathers (24 reads per record) stay L2
 // resident: LG = 512 lanes -> 3060 x 512 x 12 B = 18.8 MB for n18360.
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "block_kernels.cuh"
@@ -42,8 +43,51 @@ struct AggArgs {
   int reverse;         // visit lane groups last-to-first
   int rows_eff;        // rows the grid covers (rows / items per thread, rounded up)
   const uint32_t* active;   // early stop: lane mask words (gamma / 32) or null
-  const int32_t* done;      // early stop: this window's "all lanes frozen" flag or null
+  const uint32_t* active2;  // early stop: second mask ANDed in (active = act & bad on the fly) or null
 };
+
+// 32-lane word of the early-stop mask holding lane g0 (all on without one)
+__device__ __forceinline__ uint32_t es_word(const AggArgs& a, int g0) {
+  if (!a.active) return 0xffffffffu;
+  uint32_t w = a.active[g0 >> 5];
+  if (a.active2) w &= a.active2[g0 >> 5];
+  return w;
+}
+
+// lanes [g0, g0 + vec) of the early-stop mask
+__device__ __forceinline__ unsigned es_lanes(const AggArgs& a, int g0, int vec) {
+  return (es_word(a, g0) >> (g0 & 31)) & ((1u << vec) - 1u);
+}
+
+// early stop, per (variable n, lane vector q): the mask word, the vector's
+// active lanes, and the hard bits its frozen lanes recorded at their freeze
+// iteration (loaded up front with the item's other operands, only when some
+// lane of the vector is frozen and some lane of the word is not)
+struct EsLanes {
+  uint32_t wmask;
+  unsigned lanes, old;
+};
+
+template <int VEC>
+__device__ __forceinline__ EsLanes es_begin(const AggArgs& a, int n, int q) {
+  constexpr unsigned FULL = (1u << VEC) - 1u;
+  EsLanes e;
+  e.wmask = es_word(a, q * VEC);
+  e.lanes = (e.wmask >> ((q * VEC) & 31)) & FULL;
+  e.old = 0u;
+  if (a.hb && e.lanes != FULL && e.wmask != 0u)
+    e.old = (a.hb[(size_t)n * (a.gamma >> 5) + ((q * VEC) >> 5)] >> ((q * VEC) & 31)) & FULL & ~e.lanes;
+  return e;
+}
+
+// the hard-bit word of variable n gets the active lanes' new bits and the
+// frozen lanes' recorded ones; a word whose 32 lanes are all frozen is left
+// untouched -- so the planes always hold every lane's result and the decode
+// needs no final recompute from the posteriors
+template <int VEC>
+__device__ __forceinline__ void es_store_bits(const AggArgs& a, int n, int q, unsigned bits, const EsLanes& e) {
+  store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, (bits & e.lanes) | e.old, e.wmask != 0u);
+}
 
 // min CTAs/SM for the variable job: 4 x 256 threads caps it at 64 registers,
 // enough to issue all 17 loads of an item before its arithmetic (measured best
@@ -76,7 +120,7 @@ __device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned 
 
 template <int DC, int VEC, bool FROM_MU>
 __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid, int m, int q) {
-  if (a.active && lane_bits_of(a.active, q * VEC, VEC) == 0) return;   // frozen lanes keep stale records
+  if (a.active && es_lanes(a, q * VEC, VEC) == 0) return;   // frozen lanes keep stale records
   int jrow = 0, r = 0;
   if constexpr (FROM_MU) {
     jrow = div_p(grid, m);
@@ -135,13 +179,15 @@ template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid, int n, int q, int l,
                                             const int (&mrow)[DV], float (&tot)[VEC], float (&v2c)[DV][VEC],
                                             const float (&sS)[DV][VEC], const float (&sS2)[DV][VEC],
-                                            const float (&sM)[DV][VEC]);
+                                            const float (&sM)[DV][VEC], const EsLanes& es);
 
 template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, int n, int q) {
+  EsLanes es{0xffffffffu, (1u << VEC) - 1u, 0u};
   if constexpr ((FLAGS & AGG_ES) != 0) {
-    if (lane_bits_of(a.active, q * VEC, VEC) == 0) {   // every lane of the vector frozen
-      if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, 0u, true);
+    es = es_begin<VEC>(a, n, q);
+    if (es.lanes == 0) {   // every lane of the vector frozen
+      if (a.hb) es_store_bits<VEC>(a, n, q, 0u, es);
       return;
     }
   }
@@ -164,14 +210,14 @@ __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, i
     vload<VEC>(rec + a.gamma, sS2[j]);
     vload<VEC>(rec + 2 * a.gamma, sM[j]);
   }
-  var_compute<DV, VEC, FLAGS>(a, grid, n, q, l, mrow, tot, v2c, sS, sS2, sM);
+  var_compute<DV, VEC, FLAGS>(a, grid, n, q, l, mrow, tot, v2c, sS, sS2, sM, es);
 }
 
 template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid, int n, int q, int l,
                                             const int (&mrow)[DV], float (&tot)[VEC], float (&v2c)[DV][VEC],
                                             const float (&sS)[DV][VEC], const float (&sS2)[DV][VEC],
-                                            const float (&sM)[DV][VEC]) {
+                                            const float (&sM)[DV][VEC], const EsLanes& es) {
   float al[DV][VEC];
   if constexpr (FLAGS & AGG_FIRST) {
     // beta^0 = mu on every edge, in the phi form the fused-init check pass saw
@@ -229,8 +275,7 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
 #pragma unroll
       for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
   }
-  unsigned lanes = (1u << VEC) - 1u;
-  if constexpr ((FLAGS & AGG_ES) != 0) lanes = lane_bits_of(a.active, q * VEC, VEC);
+  const unsigned lanes = es.lanes;
   if constexpr (!(FLAGS & AGG_LAST)) {
 #pragma unroll
     for (int j = 0; j < DV; ++j) {
@@ -253,11 +298,18 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
           b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
         }
       }
+      float* dst = a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC;
       if constexpr ((FLAGS & AGG_ES) != 0) {
+        // frozen lanes keep their packages: a partially frozen vector stores its
+        // active lanes one by one (no need to keep the old packages live)
+        if (lanes != (1u << VEC) - 1u) {
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) b[i] = ((lanes >> i) & 1u) ? b[i] : v2c[j][i];   // frozen: unchanged
+          for (int i = 0; i < VEC; ++i)
+            if ((lanes >> i) & 1u) dst[i] = b[i];
+          continue;
+        }
       }
-      vstore<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, b);
+      vstore<VEC>(dst, b);
     }
   }
   if constexpr ((FLAGS & (AGG_LAST | AGG_ES)) != 0) {
@@ -268,7 +320,6 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
       pst[i] = clampL(tot[i]);
       bits |= (pst[i] < 0.0f ? 1u : 0u) << i;
     }
-    bits &= lanes;
     if (a.post) {
       if (lanes == (1u << VEC) - 1u) {
         vstore<VEC>(a.post + (size_t)n * a.gamma + q * VEC, pst);
@@ -279,7 +330,11 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
       }
     }
     // whole warps share one row (gw >= 32), so the shuffle is safe
-    if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, true);
+    if constexpr ((FLAGS & AGG_ES) != 0) {
+      if (a.hb) es_store_bits<VEC>(a, n, q, bits, es);
+    } else {
+      if (a.hb) store_bit_word<VEC>(a.hb + (size_t)n * (a.gamma >> 5), q, bits, true);
+    }
   }
 }
 
@@ -304,11 +359,13 @@ __device__ __forceinline__ void var_prefetch(const AggArgs& a, const QcGrid& gri
 // prefetched into L2 before the current one's arithmetic
 template <int DV, int VEC, int FLAGS, int ITEMS>
 __device__ __forceinline__ void var_items(const AggArgs& a, const QcGrid& grid, int n, int q) {
+  bool pf = true;
+  if constexpr ((FLAGS & AGG_ES) != 0) pf = es_lanes(a, q * VEC, VEC) != 0;   // frozen vectors fetch nothing
 #pragma unroll 1
   for (int k = 0; k < ITEMS; ++k) {
     const int nk = n + k * a.rows_eff;
     if (nk >= a.rows) break;                                   // warp-uniform (one row per warp)
-    if (k + 1 < ITEMS && nk + a.rows_eff < a.rows) var_prefetch<DV, VEC, FLAGS>(a, grid, nk + a.rows_eff, q);
+    if (pf && k + 1 < ITEMS && nk + a.rows_eff < a.rows) var_prefetch<DV, VEC, FLAGS>(a, grid, nk + a.rows_eff, q);
     var_body<DV, VEC, FLAGS>(a, grid, nk, q);
   }
 }
@@ -320,7 +377,6 @@ __global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const
   int m, q;
   const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q);
   pdl_wait();
-  if (a.done && *a.done) return;
   if (on) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
 }
 
@@ -330,24 +386,95 @@ __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggA
   int n, q;
   const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q);
   pdl_wait();
-  if (a.done && *a.done) return;
   if (on) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
 }
 
+// Early stop folded into the fused launches (bp.py:242-256).  Per-lane state,
+// word-indexed over the whole gamma, double-buffered by iteration parity:
+//   act[t & 1]  active_t = lanes still iterating after iteration t,
+//   bad[t & 1]  syndrome failures of iteration t (atomicOr),
+// so active_t = active_{t-1} & bad_t.  Launch 2t-1 = V(A, t) + C(B, t) +
+// S(B, t-1) + U(A, t); launch 2t = V(B, t) + C(A, t+1) + S(A, t) + U(B, t):
+//   V(X, t)   variable job masked by active_{t-1} = act[t&1] & bad[(t-1)&1]
+//             (both written by earlier launches; computed on the fly);
+//   C(X, t+1) check job masked by active_{t-1} (one iteration stale: records of
+//             lanes that froze at t are computed but never used);
+//   S(X, t)   syndrome of X's hard-bit planes written by V(X, t) in the
+//             previous launch -> bad[t&1] (skips words with no active lane);
+//   U(X, t)   one CTA: act[(t-1)&1] = active_{t-1}, iters_run = t-1 for the
+//             lanes that froze at t-1, clears bad[t&1] for S(X, t).
+// No launch beyond the fixed schedule's: the per-iteration syndrome / freeze
+// kernels of the two-pass early stop disappear.
+struct EsFused {
+  // S: syndrome of lane words [s_w0, s_w0 + s_W) into s_bad
+  const uint32_t* hb;        // (N, Wt) hard-bit planes
+  uint32_t* s_bad;
+  const uint32_t* s_act;     // skip words with no active lane (null: none skipped)
+  int s_w0, s_W, Wt, nbs;    // nbs = S blocks (0: no syndrome job)
+  // U: state update of lane words [u_w0, u_w0 + u_W); u_it = t (iteration of the V in this launch)
+  uint32_t* u_act_out;       // act[(t-1)&1]
+  const uint32_t* u_act_in;  // act[t&1]     (null at t = 1: every lane active)
+  const uint32_t* u_bad_in;  // bad[(t-1)&1]
+  uint32_t* u_bad_clr;       // bad[t&1]
+  int32_t* iters_run;
+  int u_w0, u_W, u_it, u_iters;   // u_W = 0: no update job
+};
+
 // One launch, two independent jobs on disjoint lane windows: the variable pass
 // of window v (compute-heavy: 2 phi per edge-lane) and the check pass of window
-// c (pure streaming).  Grid (R + 1, nbc): x = 0..R-1 are variable blocks
-// y*R + x, x = R is check block y, so the block scheduler interleaves the two
-// kinds and every SM mixes MUFU-bound and HBM-bound CTAs.
+// c (pure streaming).  Grid (R + 1, extra + nbc): after the `extra` leading
+// rows (early stop: the syndrome blocks and the one state-update block, which
+// only depend on earlier launches), x = 0..R-1 are variable blocks y*R + x and
+// x = R is check block y, so the block scheduler interleaves the two kinds and
+// every SM mixes MUFU-bound and HBM-bound CTAs.
 struct FusedArgs {
   AggArgs v, c;
-  unsigned R, nbv;                          // variable blocks per row of the grid, total
+  unsigned R, nbv, nbc;                     // variable blocks per row of the grid, total; check rows
+  unsigned es_rows;                         // leading grid rows of early-stop blocks
   unsigned v_bpg, c_bpg;                    // blocks per lane group
   unsigned long long v_magic, c_magic;      // ceil(2^40 / bpg)
+  EsFused es;
 };
 
 __device__ __forceinline__ unsigned div_magic(unsigned x, unsigned long long m) {
   return (unsigned)(((unsigned long long)x * m) >> 40);
+}
+
+// parity of check m over its d_c variables' hard bits, 32 lanes per word
+template <int DC>
+__device__ __forceinline__ void es_syndrome_block(const EsFused& e, const QcGrid& grid, unsigned blk, int M) {
+  const long long idx = (long long)blk * AGG_THREADS + threadIdx.x;
+  if (idx >= (long long)M * e.s_W) return;
+  const int m = (int)(idx / e.s_W), w = e.s_w0 + (int)(idx - (long long)m * e.s_W);
+  if (e.s_act && e.s_act[w] == 0u) return;
+  const int j = div_p(grid, m), r = m - j * grid.p;
+  uint32_t par = 0;
+#pragma unroll
+  for (int k = 0; k < DC; ++k) {
+    int c = r + grid.s[j * grid.L + k];
+    c -= (c >= grid.p) ? grid.p : 0;
+    par ^= e.hb[(size_t)(k * grid.p + c) * e.Wt + w];
+  }
+  if (par) atomicOr(e.s_bad + w, par);
+}
+
+__device__ __forceinline__ void es_update_block(const EsFused& e) {
+  for (int i = threadIdx.x; i < e.u_W; i += AGG_THREADS) {
+    const int w = e.u_w0 + i;
+    uint32_t act;
+    if (e.u_act_in) {
+      const uint32_t prev = e.u_act_in[w];
+      act = prev & e.u_bad_in[w];
+      const uint32_t froze = prev & ~act;
+      for (uint32_t f = froze; f; f &= f - 1) e.iters_run[w * 32 + __ffs(f) - 1] = e.u_it - 1;
+    } else {
+      act = 0xffffffffu;
+#pragma unroll 4
+      for (int b = 0; b < 32; ++b) e.iters_run[w * 32 + b] = e.u_iters;
+    }
+    e.u_act_out[w] = act;
+    e.u_bad_clr[w] = 0u;
+  }
 }
 
 template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
@@ -355,13 +482,18 @@ __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(Fu
   pdl_trigger();
   pdl_wait();
   int row, q;
+  if (blockIdx.y < f.es_rows) {              // early-stop bookkeeping blocks, scheduled first
+    const unsigned e = blockIdx.y * (f.R + 1) + blockIdx.x;
+    if (e < (unsigned)f.es.nbs) es_syndrome_block<DC>(f.es, grid, e, f.c.rows);
+    else if (e == (unsigned)f.es.nbs && f.es.u_W > 0) es_update_block(f.es);
+    return;
+  }
+  const unsigned y = blockIdx.y - f.es_rows;
   if (blockIdx.x == f.R) {
-    if (f.c.done && *f.c.done) return;
-    const unsigned b = blockIdx.y, g = div_magic(b, f.c_magic);
+    const unsigned b = y, g = div_magic(b, f.c_magic);
     if (agg_map(f.c, b - g * f.c_bpg, g, row, q)) check_body<DC, VC, FROM_MU>(f.c, grid, row, q);
   } else {
-    if (f.v.done && *f.v.done) return;
-    const unsigned b = blockIdx.y * f.R + blockIdx.x;
+    const unsigned b = y * f.R + blockIdx.x;
     if (b >= f.nbv) return;
     const unsigned g = div_magic(b, f.v_magic);
     if (agg_map(f.v, b - g * f.v_bpg, g, row, q)) var_items<DV, VV, FLAGS, ITEMS>(f.v, grid, row, q);
@@ -513,33 +645,44 @@ bool agg_fused_eligible(const qc_plan* p, int gamma) {
 
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
-                        const uint32_t* active, const int32_t* v_done, const int32_t* c_done, cudaStream_t s);
+                        const uint32_t* v_act, const uint32_t* v_act2, const uint32_t* c_act, const EsFused* es,
+                        cudaStream_t s);
 
 // variable pass on lanes [v0, v0 + lanes) fused with the check pass on lanes [c0, c0 + lanes)
 int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
                      const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s) {
   return launch_agg_fused_es(p, gamma, lanes, v0, flags, c0, from_mu, msgs, mu, agg, post, hb, nullptr, nullptr,
-                             nullptr, s);
+                             nullptr, nullptr, s);
 }
 
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
-                        const uint32_t* active, const int32_t* v_done, const int32_t* c_done, cudaStream_t s) {
+                        const uint32_t* v_act, const uint32_t* v_act2, const uint32_t* c_act, const EsFused* es,
+                        cudaStream_t s) {
   FusedArgs f;
   f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, AGG_REVERSE);
   f.v.rows_eff = (f.v.rows + AGG_ITEMS - 1) / AGG_ITEMS;
   f.c = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, c0, lanes, AGG_FVC, 0);
-  f.v.active = f.c.active = active;
-  f.v.done = v_done;
-  f.c.done = c_done;
+  f.v.active = v_act;
+  f.v.active2 = v_act2;
+  f.c.active = c_act;
   f.v_bpg = blocks_per_group(f.v);
   f.c_bpg = blocks_per_group(f.c);
   f.v_magic = magic40(f.v_bpg);
   f.c_magic = magic40(f.c_bpg);
   f.nbv = f.v_bpg * f.v.groups;
-  const unsigned nbc = f.c_bpg * f.c.groups;
-  f.R = (f.nbv + nbc - 1) / nbc;
-  const dim3 grid(f.R + 1, nbc, 1);
+  f.nbc = f.c_bpg * f.c.groups;
+  f.R = (f.nbv + f.nbc - 1) / f.nbc;
+  std::memset(&f.es, 0, sizeof(f.es));
+  unsigned extra = 0;
+  if (es) {
+    f.es = *es;
+    f.es.nbs = es->s_W > 0 ? (int)(((long long)p->M * es->s_W + AGG_THREADS - 1) / AGG_THREADS) : 0;
+    const unsigned jobs = (unsigned)f.es.nbs + (es->u_W > 0 ? 1u : 0u);
+    extra = (jobs + f.R) / (f.R + 1);
+  }
+  f.es_rows = extra;
+  const dim3 grid(f.R + 1, f.nbc + extra, 1);
   const QcGrid g = make_grid(p);
   int rc = (p->L == 24) ? launch_fused_dc<24, 4>(f, grid, from_mu, flags, g, s)
                         : launch_fused_dc<4, 2>(f, grid, from_mu, flags, g, s);
@@ -547,13 +690,12 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
   return check_launch("agg_fused");
 }
 
-// single passes over a lane window (active / done: early-stop mask and flag)
+// single passes over a lane window (active, active2: early-stop masks ANDed)
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active = nullptr,
-                       const int32_t* done = nullptr);
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active = nullptr);
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active = nullptr,
-                     const int32_t* done = nullptr);
+                     const uint32_t* active2 = nullptr);
 
 bool agg_eligible(const qc_plan* p) {
   return agg_mode() != 0 && p && p->qc_regular && p->E > 0 && dc_supported(p->L) && dv_supported(p->J) &&
@@ -570,11 +712,10 @@ int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, con
 }
 
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active, const int32_t* done) {
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active) {
   const int vec = pick_vec(lanes);
   AggArgs a = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, lane0, lanes, vec, 0);
   a.active = active;
-  a.done = done;
   const QcGrid g = make_grid(p);
   switch (p->L) {
     case 4: launch_check_dc<4>(a, vec, from_mu, g, s); break;
@@ -596,12 +737,12 @@ int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const fl
 
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active,
-                     const int32_t* done) {
+                     const uint32_t* active2) {
   const int vec = pick_vec_var(lanes);
   AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
                         AGG_REVERSE);
   a.active = active;
-  a.done = done;
+  a.active2 = active2;
   const QcGrid g = make_grid(p);
   switch (p->J) {
     case 2: launch_var_dv<2>(a, vec, flags, g, s); break;
@@ -656,47 +797,71 @@ int run_agg_tile(const qc_plan* p, int gamma, int lane0, int lanes, int iters, f
   return 0;
 }
 
-// Early-stop decode (bp.py:242-256) on the compact schedule: the same
-// half-iteration offset between lane halves A and B, plus each half's syndrome
-// and freeze bookkeeping (launch_es_window) right after its variable job;
-// frozen lanes keep packages / posteriors, a half whose lanes are all frozen
-// skips its jobs (done flag).  Decisions, posteriors and iteration counts equal
-// the two-pass early-stop decode (test_compact_early_stop_is_bit_identical).
-// Opt-in (QCB_AGG_ES=1): the two extra control launches per half-iteration
-// make it 7% SLOWER than the two-pass early-stop decode (profiles/r01/
-// kbench_es_compact.jsonl); it pays only once the syndrome and freeze are
-// folded into the fused launch.
-bool agg_es_eligible(const qc_plan* p, int gamma) {
-  static const int v = env_int("QCB_AGG_ES", 0);
-  return v != 0 && agg_fused_eligible(p, gamma);
-}
+// Early-stop decode (bp.py:242-256) on the compact schedule with the syndrome
+// and freeze folded into the fused launches (EsFused above): the same
+// 2 iters + 1 launches as the fixed decode, plus a 2-launch tail (last
+// syndrome, ok / iteration counts).
+// Frozen lanes keep packages and posteriors; decisions, posteriors and
+// iteration counts equal the two-pass early-stop decode bit for bit
+// (tests/test_gpu_block.py::test_compact_early_stop_is_bit_identical).
+// es = act[0] | act[1] | bad[0] | bad[1] | bad_fin, gamma/32 words each.
+bool agg_es_eligible(const qc_plan* p, int gamma) { return agg_fused_eligible(p, gamma); }
+
+int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2], uint32_t* const bad[2],
+                   uint32_t* bad_fin, uint8_t* ok, int32_t* iters_run, const float* post, uint32_t* hb,
+                   cudaStream_t s);
 
 int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
-                      uint32_t* hb, uint32_t* bad, uint32_t* active, int32_t* done, uint8_t* ok, int32_t* iters_run,
-                      cudaStream_t s) {
-  const int H = gamma / 2, A = 0, B = H;
-  int32_t* dA = done;
-  int32_t* dB = done + 1;
+                      uint32_t* hb, uint32_t* es_words, uint8_t* ok, int32_t* iters_run, cudaStream_t s) {
+  const int W = gamma / 32, H = gamma / 2, A = 0, B = H, WH = W / 2;
+  uint32_t* act[2] = {es_words, es_words + W};
+  uint32_t* bad[2] = {es_words + 2 * W, es_words + 3 * W};
+  uint32_t* bad_fin = es_words + 4 * W;
   int rc;
-  if ((rc = launch_es_start(A, H, iters, bad, active, iters_run, dA, s))) return rc;
-  if ((rc = launch_es_start(B, H, iters, bad, active, iters_run, dB, s))) return rc;
-  if ((rc = launch_agg_check_w(p, gamma, A, H, true, msgs, mu, agg, s, active, dA))) return rc;
+  cudaMemsetAsync(bad_fin, 0, sizeof(uint32_t) * W, s);
+  if ((rc = launch_agg_check_w(p, gamma, A, H, true, msgs, mu, agg, s))) return rc;
+  auto es_for = [&](int t, int vw0, int sw0, bool syn) {
+    EsFused e{};
+    e.hb = hb;
+    e.Wt = W;
+    if (syn) {                       // S(Y, t') of the half whose V ran in the previous launch
+      const int tp = (sw0 == A / 32) ? t : t - 1;    // A's syndrome lags one launch: iteration t; B's: t - 1
+      e.s_bad = bad[tp & 1];
+      e.s_act = act[(tp - 1) & 1];
+      e.s_w0 = sw0;
+      e.s_W = WH;
+    }
+    e.u_act_out = act[(t - 1) & 1];
+    e.u_act_in = t == 1 ? nullptr : act[t & 1];
+    e.u_bad_in = bad[(t - 1) & 1];
+    e.u_bad_clr = bad[t & 1];
+    e.iters_run = iters_run;
+    e.u_w0 = vw0;
+    e.u_W = WH;
+    e.u_it = t;
+    e.u_iters = iters;
+    return e;
+  };
   for (int t = 1; t <= iters; ++t) {
     const int vflags = AGG_ES | (t == 1 ? AGG_FIRST : 0) | (t == iters ? AGG_LAST : 0);
-    // var(A, t) + check(B, t), then A's syndrome / freeze
-    if ((rc = launch_agg_fused_es(p, gamma, H, A, vflags, B, t == 1, msgs, mu, agg, post, hb, active, dA, dB, s)))
+    const uint32_t* vm = t == 1 ? nullptr : act[t & 1];        // active_{t-1} = act[t&1] & bad[(t-1)&1]
+    const uint32_t* vm2 = t == 1 ? nullptr : bad[(t - 1) & 1];
+    // V(A, t) + C(B, t) + S(B, t-1) + U(A, t); C(B, t) masked by active_{t-2}(B) = act[t&1]
+    EsFused e1 = es_for(t, A / 32, B / 32, t > 1);
+    if ((rc = launch_agg_fused_es(p, gamma, H, A, vflags, B, t == 1, msgs, mu, agg, post, hb, vm, vm2,
+                                  t <= 2 ? nullptr : act[t & 1], &e1, s)))
       return rc;
-    if ((rc = launch_es_window(p, gamma, A, H, t, hb, bad, active, iters_run, dA, s))) return rc;
+    // V(B, t) + C(A, t+1) + S(A, t) + U(B, t); C(A, t+1) masked by active_{t-1}(A) = act[(t-1)&1]
+    EsFused e2 = es_for(t, B / 32, A / 32, true);
     if (t < iters) {
-      // var(B, t) + check(A, t + 1)
-      if ((rc = launch_agg_fused_es(p, gamma, H, B, vflags, A, false, msgs, mu, agg, post, hb, active, dB, dA, s)))
+      if ((rc = launch_agg_fused_es(p, gamma, H, B, vflags, A, false, msgs, mu, agg, post, hb, vm, vm2,
+                                    act[(t - 1) & 1], &e2, s)))
         return rc;
-    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, active, dB))) {
+    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, vm, vm2))) {
       return rc;
     }
-    if ((rc = launch_es_window(p, gamma, B, H, t, hb, bad, active, iters_run, dB, s))) return rc;
   }
-  return launch_es_finish(p, gamma, bad, active, ok, post, hb, s);
+  return launch_es_tail(p, gamma, iters, act, bad, bad_fin, ok, iters_run, post, hb, s);
 }
 
 int agg_decode_launches(const qc_plan* p, int gamma, int iters) {
@@ -743,8 +908,8 @@ int qc_agg_fused(const qc_plan* p, int gamma, int lanes, int var_lane0, int var_
 int qc_decode_launches(const qc_plan* p, int gamma, int iters, int early_stop) {
   if (!p || iters < 1) return -1;
   if (!early_stop && qcb::agg_eligible(p)) return 3 + qcb::agg_decode_launches(p, gamma, iters);
-  // compact early stop: 2 es_start, first check, per iteration 2 x (job + syndrome + freeze), finish (2)
-  if (early_stop && qcb::agg_es_eligible(p, gamma)) return 2 + 1 + 6 * iters + 2;
+  // compact early stop: memset, first check, 2 x iters jobs (syndrome / freeze folded in), tail (2)
+  if (early_stop && qcb::agg_es_eligible(p, gamma)) return 1 + 2 * iters + 2;
   return early_stop ? 2 + 4 * iters + 2 : 1 + 2 * iters + 2;
 }
 

@@ -55,19 +55,6 @@ __global__ void syndrome_kernel(const uint32_t* hb, uint32_t* bad, const int32_t
   if (par) atomicOr(bad + w, par);
 }
 
-// the same over the 32-lane words [w0, w0 + W) of planes with row stride Wt
-__global__ void syndrome_w_kernel(const uint32_t* hb, uint32_t* bad, const int32_t* check_ptr,
-                                  const int32_t* edge_var, int M, int Wt, int w0, int W, const int32_t* done) {
-  if (done && *done) return;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)M * W) return;
-  int m = (int)(tid / W), w = w0 + (int)(tid - (long long)m * W);
-  int e0 = check_ptr[m], deg = check_ptr[m + 1] - e0;
-  uint32_t par = 0;
-  for (int k = 0; k < deg; ++k) par ^= hb[(size_t)edge_var[e0 + k] * Wt + w];
-  if (par) atomicOr(bad + w, par);
-}
-
 __global__ void hard_bits_kernel(const float* post, uint32_t* hb, int N, int gamma) {
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   int GV = gamma / 4;
@@ -266,31 +253,46 @@ int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* 
 }  // namespace
 
 namespace qcb {
+// decode work buffer: lane-mask words (early stop: bad | active | done for the
+// two-pass path; act[2] | bad[2] | bad_fin for the compact one) padded to 64
+// words, then the check records of the compact schedule (agg.cu)
+size_t work_head_words(int gamma) {
+  const size_t W = (size_t)(gamma > 0 ? gamma : 0) / 32;
+  return (5 * W + 4 + 63) / 64 * 64;
+}
 int launch_cnu_public(const qc_plan* p, CnuArgs a, int mode, cudaStream_t s) { return launch_cnu(p, a, mode, s); }
-// early-stop bookkeeping on a lane window (compact schedule, agg.cu)
-int launch_es_window(const qc_plan* p, int gamma, int lane0, int lanes, int it, const uint32_t* hb, uint32_t* bad,
-                     uint32_t* active, int32_t* iters_run, int32_t* done, cudaStream_t s) {
-  const int Wt = gamma / 32, w0 = lane0 / 32, W = lanes / 32;
-  if (p->M > 0) {
-    long long threads = (long long)p->M * W;
-    syndrome_w_kernel<<<blocks_for(threads), THREADS, 0, s>>>(hb, bad, p->d_check_ptr, p->d_edge_var, p->M, Wt, w0, W,
-                                                              done);
+// early-stop tail of the compact decode (agg.cu run_agg_decode_es): syndrome
+// of iteration T for every lane, then per word: active_{T-1} (half A stored by
+// its last update; half B derived here, its update never ran), lanes frozen
+// at T-1 get iters_run = T-1, ok = not active after T.
+__global__ void es_final_kernel(const uint32_t* act_a, const uint32_t* act_b, const uint32_t* bad_b,
+                                const uint32_t* bad_fin, uint8_t* ok, int32_t* iters_run, int W, int WH, int T) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  uint32_t prev;
+  if (w < WH) {
+    prev = act_a[w];
+  } else if (T == 1) {
+    prev = 0xffffffffu;
+    for (int b = 0; b < 32; ++b) iters_run[w * 32 + b] = T;
+  } else {
+    const uint32_t pp = act_b[w];
+    prev = pp & bad_b[w];
+    for (uint32_t f = pp & ~prev; f; f &= f - 1) iters_run[w * 32 + __ffs(f) - 1] = T - 1;
   }
-  es_update_kernel<<<1, 256, 0, s>>>(active + w0, bad + w0, iters_run + 32 * w0, done, W, it);
-  return check_launch("es_window");
+  const uint32_t fin = prev & bad_fin[w];
+  for (int b = 0; b < 32; ++b) ok[w * 32 + b] = ((fin >> b) & 1u) ? 0 : 1;
 }
-int launch_es_start(int lane0, int lanes, int iters, uint32_t* bad, uint32_t* active, int32_t* iters_run,
-                    int32_t* done, cudaStream_t s) {
-  const int w0 = lane0 / 32, W = lanes / 32;
-  es_start_kernel<<<1, 256, 0, s>>>(active + w0, bad + w0, iters_run + 32 * w0, done, W, iters);
-  return check_launch("es_start");
-}
-int launch_es_finish(const qc_plan* p, int gamma, const uint32_t* bad, const uint32_t* active, uint8_t* ok,
-                     const float* post, uint32_t* hb, cudaStream_t s) {
-  finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, active, ok, gamma);
-  long long threads = (long long)p->N * (gamma / 4);
-  hard_bits_kernel<<<blocks_for(threads), THREADS, 0, s>>>(post, hb, p->N, gamma);
-  return check_launch("es_finish");
+
+int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2], uint32_t* const bad[2],
+                   uint32_t* bad_fin, uint8_t* ok, int32_t* iters_run, const float* post, uint32_t* hb,
+                   cudaStream_t s) {
+  const int W = gamma / 32, T = iters;
+  if (int rc = launch_syndrome(p, gamma, hb, bad_fin, nullptr, s)) return rc;
+  es_final_kernel<<<(W + 127) / 128, 128, 0, s>>>(act[(T - 1) & 1], act[T & 1], bad[(T - 1) & 1], bad_fin, ok,
+                                                   iters_run, W, W / 2, T);
+  (void)post;   // the hard-bit planes already hold every lane's recorded bits (agg.cu es_store_bits)
+  return check_launch("es_tail");
 }
 int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s) {
   return launch_syndrome(p, gamma, hb, bad, nullptr, s);
@@ -370,11 +372,10 @@ int qc_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane
 }
 
 size_t qc_decode_work_words(const qc_plan* p, int gamma) {
-  // bad (W) | active (W) | done (1) | pad to 64 words | check records (agg.cu)
-  size_t W = (size_t)(gamma > 0 ? gamma : 0) / 32;
-  size_t head = (2 * W + 4 + 63) / 64 * 64;
-  return head + agg_words(p, gamma);
+  return work_head_words(gamma) + agg_words(p, gamma);
 }
+
+size_t qc_decode_records_offset(int gamma) { return work_head_words(gamma); }
 
 int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const float* mu, float* msgs,
               float* post, uint32_t* hb, uint32_t* work, uint8_t* ok, int32_t* iters_run,
@@ -392,7 +393,7 @@ int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const floa
   // iteration 1 reads beta^0 = mu straight from the LLRs (fused init).
   if (!early_stop && agg_eligible(p)) {
     // compact check-state schedule (agg.cu): bit-identical, fewer package bytes
-    float* agg = reinterpret_cast<float*>(work + (2 * (size_t)W + 4 + 63) / 64 * 64);
+    float* agg = reinterpret_cast<float*>(work + work_head_words(gamma));
     cudaMemsetAsync(bad, 0, sizeof(uint32_t) * W, s);
     fill_i32<<<blocks_for(gamma), THREADS, 0, s>>>(iters_run, gamma, iters);
     if ((rc = run_agg_decode(p, gamma, iters, msgs, mu, agg, post, hb, s))) return rc;
@@ -413,10 +414,9 @@ int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const floa
     if ((rc = launch_syndrome(p, gamma, hb, bad, nullptr, s))) return rc;
     finalize_ok_kernel<<<blocks_for(gamma), THREADS, 0, s>>>(bad, nullptr, ok, gamma);
   } else if (agg_es_eligible(p, gamma)) {
-    // compact schedule with per-lane freezing (agg.cu); done flags per lane half
-    if ((rc = run_agg_decode_es(p, gamma, iters, msgs, mu, reinterpret_cast<float*>(
-                                    work + (2 * (size_t)W + 4 + 63) / 64 * 64),
-                                post, hb, bad, active, done, ok, iters_run, s)))
+    // compact schedule, syndrome and freeze folded into the fused launches (agg.cu)
+    if ((rc = run_agg_decode_es(p, gamma, iters, msgs, mu, reinterpret_cast<float*>(work + work_head_words(gamma)),
+                                post, hb, work, ok, iters_run, s)))
       return rc;
   } else {
     es_start_kernel<<<1, 256, 0, s>>>(active, bad, iters_run, done, W, iters);

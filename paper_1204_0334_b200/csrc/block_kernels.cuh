@@ -297,14 +297,8 @@ int run_agg_decode(const qc_plan* p, int gamma, int iters, float* msgs, const fl
 int agg_decode_launches(const qc_plan* p, int gamma, int iters);
 bool agg_es_eligible(const qc_plan* p, int gamma);
 int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
-                      uint32_t* hb, uint32_t* bad, uint32_t* active, int32_t* done, uint8_t* ok, int32_t* iters_run,
-                      cudaStream_t s);
-int launch_es_window(const qc_plan* p, int gamma, int lane0, int lanes, int it, const uint32_t* hb, uint32_t* bad,
-                     uint32_t* active, int32_t* iters_run, int32_t* done, cudaStream_t s);
-int launch_es_start(int lane0, int lanes, int iters, uint32_t* bad, uint32_t* active, int32_t* iters_run,
-                    int32_t* done, cudaStream_t s);
-int launch_es_finish(const qc_plan* p, int gamma, const uint32_t* bad, const uint32_t* active, uint8_t* ok,
-                     const float* post, uint32_t* hb, cudaStream_t s);
+                      uint32_t* hb, uint32_t* es_words, uint8_t* ok, int32_t* iters_run, cudaStream_t s);
+size_t work_head_words(int gamma);
 bool agg_fused_eligible(const qc_plan* p, int gamma);
 int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
                      const float* mu, float* agg, float* post, uint32_t* hb, cudaStream_t s);

@@ -305,33 +305,37 @@ sys.path.insert(0, '.')
 import paper_1204_0334_b200 as q
 h, exp = q.load_code(q.codes.bundled_code_path('n18360'))
 lay = q.build_edge_layout(h)
-y = q.simulate_block(q.ChannelConfig(float(sys.argv[2]), 5 / 6, seed=6, gamma=512), lay.n_vars)
-r = q.decode_batch(lay, y, q.ebn0_to_sigma(float(sys.argv[2]), 5 / 6), 30, early_stop=True)
+G, it = int(sys.argv[3]), int(sys.argv[4])
+y = q.simulate_block(q.ChannelConfig(float(sys.argv[2]), 5 / 6, seed=6, gamma=G), lay.n_vars)
+r = q.decode_batch(lay, y, q.ebn0_to_sigma(float(sys.argv[2]), 5 / 6), it, early_stop=True)
 np.savez(sys.argv[1], post=r.posteriors, bits=r.hard_bits, ok=r.syndrome_ok, its=r.iterations_run)
 """
 
 
 def test_compact_early_stop_is_bit_identical(gpu, tmp_path):
-    """Early-stop decode on the compact schedule (QCB_AGG_ES=1, default) equals the
-    two-pass early-stop decode bit for bit: posteriors captured at the freeze
-    iteration, hard bits, syndrome flags, iteration counts -- at an SNR where
-    lanes freeze at many different iterations and one where half the frames fail."""
+    """Early-stop decode on the compact schedule (default for regular (4, 24)
+    grids at gamma % 256 == 0: syndrome and freeze folded into the fused
+    launches) equals the two-pass early-stop decode (QCB_AGG=0) bit for bit:
+    posteriors captured at the freeze iteration, hard bits, syndrome flags,
+    iteration counts -- where lanes freeze at many different iterations, where
+    half the frames fail, and for the 1- and 2-iteration edge cases of the
+    launch sequence."""
     import os
     import subprocess
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for db in ("3.2", "2.9"):
+    for db, G, it in (("3.2", 512, 30), ("2.9", 512, 30), ("3.6", 256, 1), ("3.6", 256, 2), ("3.4", 768, 7)):
         outs = []
-        for env in ({"QCB_AGG_ES": "0"}, {"QCB_AGG_ES": "1"}, {"QCB_AGG": "0"}):
-            f = tmp_path / f"es{db}_{len(outs)}.npz"
-            subprocess.run([sys.executable, "-c", _ES_SNIPPET, str(f), db], cwd=repo, check=True,
-                           env={**os.environ, **env})
+        for env in ({"QCB_AGG": "0"}, {}):
+            f = tmp_path / f"es{db}_{G}_{it}_{len(outs)}.npz"
+            subprocess.run([sys.executable, "-c", _ES_SNIPPET, str(f), db, str(G), str(it)], cwd=repo,
+                           check=True, env={**os.environ, **env})
             outs.append(np.load(f))
         its = outs[0]["its"]
-        assert its.min() < its.max()                       # lanes froze at different iterations
-        for o in outs[1:]:
-            for k in ("post", "bits", "ok", "its"):
-                assert np.array_equal(outs[0][k], o[k]), (db, k)
+        if it == 30:
+            assert its.min() < its.max()                       # lanes froze at different iterations
+        for k in ("post", "bits", "ok", "its"):
+            assert np.array_equal(outs[0][k], outs[1][k]), (db, G, it, k)
 
 
 def test_graded_chunk_plans_agree(gpu, monkeypatch):

@@ -56,7 +56,7 @@ def main():
                                            None, None, st))
         agg_ms = {}
         W = G // 32
-        agg_ptr = dec.work.data_ptr() + ((2 * W + 4 + 63) // 64 * 64) * 4
+        agg_ptr = dec.work.data_ptr() + int(_lib.load().qc_decode_records_offset(G)) * 4
         if os.environ.get("QCB_AGG", "1") != "0" and lay.check_regular:
             agg_ms["agg_check_ms"] = timeit(lambda: _lib.call("qc_agg_check", p, G, 0, dec.msgs.data_ptr(),
                                                               dec.mu.data_ptr(), agg_ptr, st))
