@@ -69,30 +69,35 @@ __global__ void hard_bits_kernel(const float* post, uint32_t* hb, int N, int gam
   store_bit_word<4>(hb + (size_t)n * (gamma >> 5), q, bits, valid);
 }
 
-// per-lane popcount over variables: block (word w, variable chunk)
-__global__ void bit_errors_kernel(const uint32_t* hb, int32_t* lane_bits, int N, int W) {
-  __shared__ int cnt[32];
-  int w = blockIdx.y;
-  if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+// per-lane popcount over the N hard-bit planes (lane_bits must be zeroed):
+// each block walks a chunk of variables with consecutive threads on
+// consecutive 32-lane words (coalesced), counts set bits in shared memory
+// (hard bits are sparse at useful SNRs: a zero word costs one load), and adds
+// its nonzero lane counts to the global ones
+__global__ void bit_errors_kernel(const uint32_t* hb, int32_t* lane_bits, int N, int W, int rows_per_block) {
+  extern __shared__ int cnt[];                 // W * 32 counters
+  for (int i = threadIdx.x; i < W * 32; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
-  int c[32];
+  const int n0 = blockIdx.x * rows_per_block, n1 = min(N, n0 + rows_per_block);
+  const long long total = (long long)(n1 - n0) * W;
+  const uint32_t* base = hb + (size_t)n0 * W;               // the block's rows are contiguous words
+  constexpr int U = 8;                                       // independent loads in flight per thread
+  for (long long i0 = threadIdx.x; i0 < total; i0 += (long long)U * blockDim.x) {
+    uint32_t x[U];
 #pragma unroll
-  for (int b = 0; b < 32; ++b) c[b] = 0;
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    uint32_t x = hb[(size_t)n * W + w];
-    if (x) {
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + (long long)u * blockDim.x;
+      x[u] = i < total ? base[i] : 0u;
+    }
 #pragma unroll
-      for (int b = 0; b < 32; ++b) c[b] += (x >> b) & 1u;
+    for (int u = 0; u < U; ++u) {
+      const int w = (int)((i0 + (long long)u * blockDim.x) % W);
+      for (uint32_t v = x[u]; v; v &= v - 1) atomicAdd(&cnt[w * 32 + __ffs(v) - 1], 1);
     }
   }
-#pragma unroll
-  for (int b = 0; b < 32; ++b) {
-    int v = c[b];
-    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cnt[b], v);
-  }
   __syncthreads();
-  if (threadIdx.x < 32 && cnt[threadIdx.x]) atomicAdd(lane_bits + w * 32 + threadIdx.x, cnt[threadIdx.x]);
+  for (int i = threadIdx.x; i < W * 32; i += blockDim.x)
+    if (cnt[i]) atomicAdd(lane_bits + i, cnt[i]);
 }
 
 // early-stop bookkeeping after iteration `it` (bp.py:242-256): lanes that are
@@ -242,11 +247,19 @@ int launch_syndrome(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* b
 }
 
 int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s) {
-  int W = gamma / 32;
+  const int W = gamma / 32;
   cudaMemsetAsync(lane_bits, 0, sizeof(int32_t) * gamma, s);
-  int chunks = std::max(1, std::min(64, (p->N + 255) / 256));
-  dim3 grid(chunks, W);
-  bit_errors_kernel<<<grid, 256, 0, s>>>(hb, lane_bits, p->N, W);
+  if (p->N == 0) return 0;
+  // ~2 blocks per SM, each at least 64 rows; W * 32 counters of shared memory
+  const int blocks = std::max(1, std::min(296, (p->N + 63) / 64));
+  const int rows = (p->N + blocks - 1) / blocks;
+  const size_t smem = (size_t)W * 32 * sizeof(int);
+  static const bool big_smem = [] {     // once per process (not a stream operation: graph-capture safe)
+    return cudaFuncSetAttribute(bit_errors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ==
+           cudaSuccess;
+  }();
+  if (smem > (big_smem ? 200u : 48u) * 1024) return fail_arg("bit_errors: gamma too large for the shared counters");
+  bit_errors_kernel<<<(p->N + rows - 1) / rows, 256, smem, s>>>(hb, lane_bits, p->N, W, rows);
   return check_launch("bit_errors");
 }
 

@@ -16,8 +16,8 @@
 //
 // Codeword id k of this rank is reference batch b = (k / gref) * W + rank,
 // lane lane_base + b * gref + k % gref (batches round-robin over W ranks).
-// Tick = fresh-group channel -> fresh-group init -> check pass -> variable
-// pass -> syndrome -> per-lane bit counts -> finish (count, freeze, reassign).
+// Tick = fresh groups' channel + init -> check pass -> variable pass ->
+// syndrome -> per-lane bit counts -> finish (count, freeze, reassign).
 #include <cuda_runtime.h>
 
 #include "block_kernels.cuh"
@@ -81,8 +81,13 @@ __global__ void rc_init_kernel(RcState s, RcConfig c) {
   }
 }
 
-// channel LLRs of the fresh groups: item = (fresh group, Philox block, lane in group)
-__global__ void __launch_bounds__(THREADS) rc_channel_kernel(RcState s, RcConfig c, float* mu, int n) {
+// channel LLRs of the fresh groups and their beta^0 = mu packages in phi form,
+// in one pass: item = (fresh group, Philox block of 4 positions, lane in
+// group).  Each (variable, lane) value is written to mu and to the J edges of
+// the variable (QC arithmetic, codes.py:159-178); the 8 lanes of a group are
+// consecutive threads, so every write fills whole 32-byte sectors.
+__global__ void __launch_bounds__(THREADS) rc_fresh_kernel(RcState s, RcConfig c, const __grid_constant__ QcGrid grid,
+                                                           float* mu, float* msgs, int n) {
   const int F = *s.fresh_count;
   const long long nblk = (n + 3) / 4;
   const long long items = (long long)F * nblk * GROUP;
@@ -104,32 +109,16 @@ __global__ void __launch_bounds__(THREADS) rc_channel_kernel(RcState s, RcConfig
       double y = __dadd_rn(1.0, __dmul_rn(c.sigma, ndtri_cephes(word_to_uniform(w[q]))));
       double m = __ddiv_rn(__dmul_rn(2.0, y), s2);
       m = m < -50.0 ? -50.0 : (m > 50.0 ? 50.0 : m);
-      mu[(size_t)pos * c.gamma + g] = __double2float_rn(m);
+      const float mf = __double2float_rn(m);
+      mu[(size_t)pos * c.gamma + g] = mf;
+      const float ps = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(mf))) | (__float_as_uint(mf) & 0x80000000u));
+      const int vb = div_p(grid, (int)pos), cc = (int)pos - vb * grid.p;
+      for (int j = 0; j < grid.J; ++j) {
+        int rr = cc - grid.s[j * grid.L + vb];
+        rr += (rr < 0) ? grid.p : 0;
+        msgs[((size_t)(j * grid.p + rr) * grid.L + vb) * c.gamma + g] = ps;
+      }
     }
-  }
-}
-
-// beta^0 = mu in phi form for the fresh groups: item = (fresh group, edge, half group)
-__global__ void __launch_bounds__(THREADS) rc_seed_kernel(RcState s, const __grid_constant__ QcGrid grid,
-                                                          const float* mu, float* msgs, int E, int gamma) {
-  const int F = *s.fresh_count;
-  const long long items = (long long)F * E * 2;
-  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (long long)gridDim.x * blockDim.x) {
-    const int h = (int)(it & 1);
-    const long long r = it >> 1;
-    const int e = (int)(r % E);
-    const int g0 = s.fresh_list[r / E] * GROUP + 4 * h;
-    const int m = e / grid.L, l = e - m * grid.L;
-    const int j = m / grid.p, rr = m - j * grid.p;
-    int cc = rr + grid.s[j * grid.L + l];
-    cc -= (cc >= grid.p) ? grid.p : 0;
-    float v[4];
-    vload<4>(mu + (size_t)(l * grid.p + cc) * gamma + g0, v);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      v[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(v[i]))) | (__float_as_uint(v[i]) & 0x80000000u));
-    vstore<4>(msgs + (size_t)e * gamma + g0, v);
   }
 }
 
@@ -242,8 +231,7 @@ int qc_rc_ticks(const qc_plan* p, int gamma, int gamma_ref, int world, int rank,
   const unsigned persist = (unsigned)nsm * (2048 / THREADS);   // 2048 threads per SM
   int rc;
   for (int t = 0; t < ticks; ++t) {
-    rc_channel_kernel<<<persist, THREADS, 0, st>>>(s, c, mu, p->N);
-    rc_seed_kernel<<<persist, THREADS, 0, st>>>(s, g, mu, msgs, p->E, gamma);
+    rc_fresh_kernel<<<persist, THREADS, 0, st>>>(s, c, g, mu, msgs, p->N);
     rc_reset_fresh_kernel<<<1, 1, 0, st>>>(s.fresh_count);
     CnuArgs a{msgs, mu, p->d_check_ptr, p->d_edge_var, s.active, nullptr, p->M, gamma};
     if ((rc = launch_cnu_public(p, a, CNU_PHI, st))) return rc;

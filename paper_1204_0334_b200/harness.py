@@ -280,8 +280,11 @@ class RecycleCampaign:
         counts = torch.zeros((n_batches + W, 3), dtype=torch.int64, device=self.mu.device)
         _lib.call("qc_rc_init", self.gk, int(id_limit), self.state.data_ptr(), _lib.stream_handle())
         self._graph = None
-        # only a window of batches after the consumed prefix can be in flight
-        win = 4 * (self.gk // gref + 1) * W + 64
+        # only a window of batches after the consumed prefix can be in flight: a
+        # graph of TICKS ticks completes at most TICKS lane generations (a codeword
+        # takes >= 1 tick) and the read window lags one round behind the consumed
+        # prefix (the look-ahead round is queued before the current one is read)
+        win = 2 * self.TICKS * (self.gk // gref + 1) * W + 64
 
         def launch(lo):
             """Queue one graph of ticks, then the reduced rows [lo, lo + win) to
