@@ -138,23 +138,58 @@ __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid,
     }
   }
   float oS[VEC], oS2[VEC], oM[VEC];
+  if constexpr (VEC % 2 == 0 && !FROM_MU) {
+    // lane pairs: the two running sums on the packed fp32 pipe (each lane
+    // rounded exactly like the scalar form below; compares / selects per lane)
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    unsigned par = 0;
-    float S = 0.0f, S2 = 0.0f, mx = -1.0f;
+    for (int i = 0; i < VEC; i += 2) {
+      unsigned par0 = 0, par1 = 0;
+      f2 S = splat2(0.0f), S2 = splat2(0.0f);
+      float mx0 = -1.0f, mx1 = -1.0f;
 #pragma unroll
-    for (int k = 0; k < DC; ++k) {
-      float b = x[k][i];
-      unsigned sb = __float_as_uint(b) & 0x80000000u;
-      float f = FROM_MU ? psi_of_nat(fabsf(b)) : fabsf(b);
-      par ^= sb;
-      S2 = (f > mx) ? S : __fadd_rn(S2, f);
-      mx = fmaxf(mx, f);
-      S = __fadd_rn(S, f);
+      for (int k = 0; k < DC; ++k) {
+        const unsigned u0 = __float_as_uint(x[k][i]), u1 = __float_as_uint(x[k][i + 1]);
+        const float f0 = __uint_as_float(u0 & 0x7fffffffu), f1 = __uint_as_float(u1 & 0x7fffffffu);
+        par0 ^= u0;
+        par1 ^= u1;
+        const f2 fp = mk2(f0, f1);
+        float s0, s1, a0, a1;
+        get2(S, s0, s1);
+        get2(add2(S2, fp), a0, a1);
+        S2 = mk2((f0 > mx0) ? s0 : a0, (f1 > mx1) ? s1 : a1);
+        mx0 = fmaxf(mx0, f0);
+        mx1 = fmaxf(mx1, f1);
+        S = add2(S, fp);
+      }
+      float s0, s1, t0, t1;
+      get2(S, s0, s1);
+      get2(S2, t0, t1);
+      oS[i] = __uint_as_float(__float_as_uint(s0) | (par0 & 0x80000000u));
+      oS[i + 1] = __uint_as_float(__float_as_uint(s1) | (par1 & 0x80000000u));
+      oS2[i] = t0;
+      oS2[i + 1] = t1;
+      oM[i] = mx0;
+      oM[i + 1] = mx1;
     }
-    oS[i] = __uint_as_float(__float_as_uint(S) | par);
-    oS2[i] = S2;
-    oM[i] = mx;
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      unsigned par = 0;
+      float S = 0.0f, S2 = 0.0f, mx = -1.0f;
+#pragma unroll
+      for (int k = 0; k < DC; ++k) {
+        float b = x[k][i];
+        unsigned sb = __float_as_uint(b) & 0x80000000u;
+        float f = FROM_MU ? psi_of_nat(fabsf(b)) : fabsf(b);
+        par ^= sb;
+        S2 = (f > mx) ? S : __fadd_rn(S2, f);
+        mx = fmaxf(mx, f);
+        S = __fadd_rn(S, f);
+      }
+      oS[i] = __uint_as_float(__float_as_uint(S) | par);
+      oS2[i] = S2;
+      oM[i] = mx;
+    }
   }
   float* rec = a.agg + (size_t)m * 3 * a.gamma + q * VEC;
   vstore<VEC>(rec, oS);
@@ -285,17 +320,18 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
         for (int i = 0; i < VEC; i += 2) {
           float d0, d1;
           get2(sub2(mk2(tot[i], tot[i + 1]), mk2(al[j][i], al[j][i + 1])), d0, d1);
-          const float be0 = clampL(d0), be1 = clampL(d1);
+          // psi(|clip(beta, +-L_MAX)|) with beta's sign (clipping never flips a sign)
           float q0, q1;
-          get2(psi_of_nat2(mk2(fabsf(be0), fabsf(be1))), q0, q1);
-          b[i] = __uint_as_float(__float_as_uint(q0) | (__float_as_uint(be0) & 0x80000000u));
-          b[i + 1] = __uint_as_float(__float_as_uint(q1) | (__float_as_uint(be1) & 0x80000000u));
+          get2(psi_of_nat_fast2(mk2(fminf(fabsf(d0), L_MAX), fminf(fabsf(d1), L_MAX))), q0, q1);
+          b[i] = __uint_as_float(__float_as_uint(q0) | (__float_as_uint(d0) & 0x80000000u));
+          b[i + 1] = __uint_as_float(__float_as_uint(q1) | (__float_as_uint(d1) & 0x80000000u));
         }
       } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-          float beta = clampL(__fsub_rn(tot[i], al[j][i]));
-          b[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) | (__float_as_uint(beta) & 0x80000000u));
+          const float d = __fsub_rn(tot[i], al[j][i]);
+          b[i] = __uint_as_float(__float_as_uint(psi_of_nat_fast(fminf(fabsf(d), L_MAX))) |
+                                 (__float_as_uint(d) & 0x80000000u));
         }
       }
       float* dst = a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC;

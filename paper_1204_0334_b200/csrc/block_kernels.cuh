@@ -233,11 +233,10 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
             for (int i = 0; i < VEC; i += 2) {
               float d0, d1;
               get2(sub2(mk2(tot[i], tot[i + 1]), mk2(am[j][i], am[j][i + 1])), d0, d1);
-              const float be0 = clampL(d0), be1 = clampL(d1);
               float q0, q1;
-              get2(psi_of_nat2(mk2(fabsf(be0), fabsf(be1))), q0, q1);
-              q0 = __uint_as_float(__float_as_uint(q0) | (__float_as_uint(be0) & 0x80000000u));
-              q1 = __uint_as_float(__float_as_uint(q1) | (__float_as_uint(be1) & 0x80000000u));
+              get2(psi_of_nat_fast2(mk2(fminf(fabsf(d0), L_MAX), fminf(fabsf(d1), L_MAX))), q0, q1);
+              q0 = __uint_as_float(__float_as_uint(q0) | (__float_as_uint(d0) & 0x80000000u));
+              q1 = __uint_as_float(__float_as_uint(q1) | (__float_as_uint(d1) & 0x80000000u));
               b[i] = ((lanes >> i) & 1u) ? q0 : am[j][i];
               b[i + 1] = ((lanes >> (i + 1)) & 1u) ? q1 : am[j][i + 1];
             }
@@ -246,7 +245,7 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
             for (int i = 0; i < VEC; ++i) {
               float beta = clampL(__fsub_rn(tot[i], am[j][i]));
               if constexpr (MODE == VNU_PHI)
-                beta = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(beta))) |
+                beta = __uint_as_float(__float_as_uint(psi_of_nat_fast(fabsf(beta))) |
                                        (__float_as_uint(beta) & 0x80000000u));
               b[i] = ((lanes >> i) & 1u) ? beta : am[j][i];
             }
