@@ -4,24 +4,28 @@
 // The reference alternates check_node_update / variable_node_update over one
 // (E, gamma) package store (bp.py:134-188): the check pass reads and rewrites
 // every package, the variable pass gathers them again -- 4E + N package
-// transfers per iteration.  A check's outgoing messages are a function of four
+// transfers per iteration.  A check's outgoing messages are a function of two
 // per-(check, lane) numbers and of each edge's own incoming message:
-//     S   = sum_k psi_k            (psi = phi(|beta|)/ln2, the phi form)
+//     S   = sum_k psi_k            (psi = phi(|beta|)/ln2, the phi form), with
+//           the sign parity par = XOR of the signs in its sign bit
 //     S2  = S without its first maximum (accumulated directly: no cancellation)
-//     mx  = max_k psi_k
-//     par = XOR of the signs
-//     alpha_k = sign(par ^ sign_k) * min(phi((psi_k == mx) ? S2 : S - psi_k), cap)
-// so the check pass here writes only (S|par, S2, mx) per check and lane
-// (3 words instead of d_c packages), and the variable pass re-derives alpha_k
-// from them and the package it is about to overwrite.  The arithmetic is the
-// same instruction sequence as cnu_core + vnu_kernel (block_kernels.cuh), so
-// results are bit-identical to the two-pass schedule; the package store
-// traffic drops from 4E + N to 3E + N (+ 6M) words per lane and iteration.
+//     alpha_k = sign(par ^ sign_k) * min(phi(psi_k > S - psi_k ? S2 : S - psi_k), cap)
+// (an edge holding more than half of S is the unique maximum: it takes the
+// exclusive sum S2; for every other edge S - psi_k >= S/2 >= psi_k, so the
+// subtraction never cancels).  So the check pass writes only (S|par, S2) per
+// check and lane (2 words instead of d_c packages), and the variable pass
+// re-derives alpha_k from S|par and the package it is about to overwrite,
+// reading S2 only for dominant edges (a few % of the edge-vectors): the record
+// gathers -- 24 per record and iteration, half of the pass's L2 traffic -- stay
+// at one field.  The arithmetic is the same instruction sequence as cnu_core +
+// vnu_kernel (block_kernels.cuh), so results are bit-identical to the two-pass
+// schedule; the package store traffic drops from 4E + N to 3E + N (+ 4M)
+// words per lane and iteration.
 //
 // Thread mapping (both passes): lane-group major -- all rows (checks or
 // variables) of lanes [g*LG, (g+1)*LG) before the next lane group, so the
 // check records a variable pass gathers (24 reads per record) stay L2
-// resident: LG = 512 lanes -> 3060 x 512 x 12 B = 18.8 MB for n18360.
+// resident: LG = 128 lanes -> 3060 x 128 x 8 B = 3.1 MB for n18360.
 #include <cstdlib>
 #include <cstring>
 #include <utility>
@@ -30,10 +34,14 @@
 
 namespace qcb {
 
+// check record fields per (check, lane): S|par (sum of psi, sign parity in the
+// sign bit) and S2 (the sum without its first maximum)
+constexpr int AGG_FIELDS = 2;
+
 struct AggArgs {
   float* msgs;         // (E, gamma) phi-form var->check packages
   const float* mu;     // (N, gamma) channel LLRs
-  float* agg;          // (M, 3, gamma): S|par, S2, mx
+  float* agg;          // (M, AGG_FIELDS, gamma): S|par, S2
   float* post;         // (N, gamma) or null
   uint32_t* hb;        // (N, gamma/32) or null
   int rows, gamma;     // rows = M (check pass) or N (variable pass); gamma = row stride in lanes
@@ -137,7 +145,7 @@ __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid,
       vload<VEC>(a.msgs + (size_t)(m * DC + k) * a.gamma + q * VEC, x[k]);
     }
   }
-  float oS[VEC], oS2[VEC], oM[VEC];
+  float oS[VEC], oS2[VEC];
   if constexpr (VEC % 2 == 0 && !FROM_MU) {
     // lane pairs: the two running sums on the packed fp32 pipe (each lane
     // rounded exactly like the scalar form below; compares / selects per lane)
@@ -168,8 +176,6 @@ __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid,
       oS[i + 1] = __uint_as_float(__float_as_uint(s1) | (par1 & 0x80000000u));
       oS2[i] = t0;
       oS2[i + 1] = t1;
-      oM[i] = mx0;
-      oM[i + 1] = mx1;
     }
   } else {
 #pragma unroll
@@ -188,13 +194,11 @@ __device__ __forceinline__ void check_body(const AggArgs& a, const QcGrid& grid,
       }
       oS[i] = __uint_as_float(__float_as_uint(S) | par);
       oS2[i] = S2;
-      oM[i] = mx;
     }
   }
-  float* rec = a.agg + (size_t)m * 3 * a.gamma + q * VEC;
+  float* rec = a.agg + (size_t)m * AGG_FIELDS * a.gamma + q * VEC;
   vstore<VEC>(rec, oS);
   vstore<VEC>(rec + a.gamma, oS2);
-  vstore<VEC>(rec + 2 * a.gamma, oM);
 }
 
 // check-record rows of variable n (block column l, circulant row c)
@@ -213,8 +217,7 @@ __device__ __forceinline__ int var_rows(const QcGrid& grid, int n, int (&mrow)[D
 template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid, int n, int q, int l,
                                             const int (&mrow)[DV], float (&tot)[VEC], float (&v2c)[DV][VEC],
-                                            const float (&sS)[DV][VEC], const float (&sS2)[DV][VEC],
-                                            const float (&sM)[DV][VEC], const EsLanes& es);
+                                            const float (&sS)[DV][VEC], const EsLanes& es);
 
 template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, int n, int q) {
@@ -236,23 +239,52 @@ __device__ __forceinline__ void var_body(const AggArgs& a, const QcGrid& grid, i
       vload<VEC>(a.msgs + ((size_t)mrow[j] * grid.L + l) * a.gamma + q * VEC, v2c[j]);
   }
   // every load of the item is issued before any arithmetic (one memory round
-  // trip per item; the compiler otherwise interleaves them with the phi math)
-  float sS[DV][VEC], sS2[DV][VEC], sM[DV][VEC];
+  // trip per item; the compiler otherwise interleaves them with the phi math);
+  // of the check records only S|par -- S2 is fetched for dominant edges only
+  float sS[DV][VEC];
 #pragma unroll
-  for (int j = 0; j < DV; ++j) {
-    const float* rec = a.agg + (size_t)mrow[j] * 3 * a.gamma + q * VEC;
-    vload<VEC>(rec, sS[j]);
-    vload<VEC>(rec + a.gamma, sS2[j]);
-    vload<VEC>(rec + 2 * a.gamma, sM[j]);
+  for (int j = 0; j < DV; ++j) vload<VEC>(a.agg + (size_t)mrow[j] * AGG_FIELDS * a.gamma + q * VEC, sS[j]);
+  var_compute<DV, VEC, FLAGS>(a, grid, n, q, l, mrow, tot, v2c, sS, es);
+}
+
+// |alpha_k| arguments of edge j for the VEC lanes: mag = S - psi_k, except for
+// the dominant edge (psi_k > S - psi_k: it holds more than half the sum, so it
+// is the unique maximum), whose exclusive sum S2 comes from the record's second
+// field -- loaded only when some lane of the vector needs it (a few % of the
+// edge-vectors), which keeps the 24-fold record gathers at one field.
+template <int VEC>
+__device__ __forceinline__ void edge_mags(const AggArgs& a, int mrow_j, int q, const float (&v2c_j)[VEC],
+                                          const float (&sS_j)[VEC], float (&mag)[VEC]) {
+  unsigned dom = 0;
+  if constexpr (VEC % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < VEC; i += 2) {
+      const float f0 = fabsf(v2c_j[i]), f1 = fabsf(v2c_j[i + 1]);
+      get2(sub2(mk2(fabsf(sS_j[i]), fabsf(sS_j[i + 1])), mk2(f0, f1)), mag[i], mag[i + 1]);
+      dom |= ((f0 > mag[i]) ? 1u : 0u) << i;
+      dom |= ((f1 > mag[i + 1]) ? 1u : 0u) << (i + 1);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const float f = fabsf(v2c_j[i]);
+      mag[i] = __fsub_rn(fabsf(sS_j[i]), f);
+      dom |= ((f > mag[i]) ? 1u : 0u) << i;
+    }
   }
-  var_compute<DV, VEC, FLAGS>(a, grid, n, q, l, mrow, tot, v2c, sS, sS2, sM, es);
+  if (dom) {
+    float s2[VEC];
+    vload<VEC>(a.agg + ((size_t)mrow_j * AGG_FIELDS + 1) * a.gamma + q * VEC, s2);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+      if ((dom >> i) & 1u) mag[i] = s2[i];
+  }
 }
 
 template <int DV, int VEC, int FLAGS>
 __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid, int n, int q, int l,
                                             const int (&mrow)[DV], float (&tot)[VEC], float (&v2c)[DV][VEC],
-                                            const float (&sS)[DV][VEC], const float (&sS2)[DV][VEC],
-                                            const float (&sM)[DV][VEC], const EsLanes& es) {
+                                            const float (&sS)[DV][VEC], const EsLanes& es) {
   float al[DV][VEC];
   if constexpr (FLAGS & AGG_FIRST) {
     // beta^0 = mu on every edge, in the phi form the fused-init check pass saw
@@ -264,51 +296,49 @@ __device__ __forceinline__ void var_compute(const AggArgs& a, const QcGrid& grid
       for (int j = 0; j < DV; ++j) v2c[j][i] = p0;
     }
   }
-  if constexpr (VEC % 2 == 0) {
-    // lane pairs on the packed fp32 pipe: bit-identical to the scalar path below
+  {
+    if constexpr (VEC % 2 == 0) {
+      // lane pairs on the packed fp32 pipe: bit-identical to the scalar path below
 #pragma unroll
-    for (int j = 0; j < DV; ++j) {
+      for (int j = 0; j < DV; ++j) {
+        float mag[VEC];
+        edge_mags<VEC>(a, mrow[j], q, v2c[j], sS[j], mag);
+#pragma unroll
+        for (int i = 0; i < VEC; i += 2) {
+          const unsigned u0 = __float_as_uint(v2c[j][i]), u1 = __float_as_uint(v2c[j][i + 1]);
+          const unsigned s0 = __float_as_uint(sS[j][i]), s1 = __float_as_uint(sS[j][i + 1]);
+          float p0, p1;
+          get2(phi_of_log2_2(mk2(mag[i], mag[i + 1])), p0, p1);
+          al[j][i] = __uint_as_float(__float_as_uint(fminf(p0, ALPHA_CAP)) | ((u0 ^ s0) & 0x80000000u));
+          al[j][i + 1] = __uint_as_float(__float_as_uint(fminf(p1, ALPHA_CAP)) | ((u1 ^ s1) & 0x80000000u));
+        }
+      }
+      // running total in increasing edge order (bp.py:179-181)
 #pragma unroll
       for (int i = 0; i < VEC; i += 2) {
-        const unsigned u0 = __float_as_uint(v2c[j][i]), u1 = __float_as_uint(v2c[j][i + 1]);
-        const unsigned s0 = __float_as_uint(sS[j][i]), s1 = __float_as_uint(sS[j][i + 1]);
-        const float f0 = __uint_as_float(u0 & 0x7fffffffu), f1 = __uint_as_float(u1 & 0x7fffffffu);
-        float d0, d1;
-        get2(sub2(mk2(__uint_as_float(s0 & 0x7fffffffu), __uint_as_float(s1 & 0x7fffffffu)), mk2(f0, f1)), d0, d1);
-        const f2 mag = mk2((f0 == sM[j][i]) ? sS2[j][i] : d0, (f1 == sM[j][i + 1]) ? sS2[j][i + 1] : d1);
-        float p0, p1;
-        get2(phi_of_log2_2(mag), p0, p1);
-        al[j][i] = __uint_as_float(__float_as_uint(fminf(p0, ALPHA_CAP)) | ((u0 ^ s0) & 0x80000000u));
-        al[j][i + 1] = __uint_as_float(__float_as_uint(fminf(p1, ALPHA_CAP)) | ((u1 ^ s1) & 0x80000000u));
+        f2 t = mk2(tot[i], tot[i + 1]);
+#pragma unroll
+        for (int j = 0; j < DV; ++j) t = add2(t, mk2(al[j][i], al[j][i + 1]));
+        get2(t, tot[i], tot[i + 1]);
       }
-    }
-    // running total in increasing edge order (bp.py:179-181)
+    } else {
 #pragma unroll
-    for (int i = 0; i < VEC; i += 2) {
-      f2 t = mk2(tot[i], tot[i + 1]);
+      for (int j = 0; j < DV; ++j) {
+        float mag[VEC];
+        edge_mags<VEC>(a, mrow[j], q, v2c[j], sS[j], mag);
 #pragma unroll
-      for (int j = 0; j < DV; ++j) t = add2(t, mk2(al[j][i], al[j][i + 1]));
-      get2(t, tot[i], tot[i + 1]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < DV; ++j) {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        unsigned u = __float_as_uint(v2c[j][i]);
-        unsigned sp = __float_as_uint(sS[j][i]);
-        float f = __uint_as_float(u & 0x7fffffffu);
-        float S = __uint_as_float(sp & 0x7fffffffu);
-        float mag = (f == sM[j][i]) ? sS2[j][i] : __fsub_rn(S, f);
-        float al_ = fminf(phi_of_log2(mag), ALPHA_CAP);
-        al[j][i] = __uint_as_float(__float_as_uint(al_) | ((u ^ sp) & 0x80000000u));
+        for (int i = 0; i < VEC; ++i) {
+          const unsigned u = __float_as_uint(v2c[j][i]), sp = __float_as_uint(sS[j][i]);
+          const float al_ = fminf(phi_of_log2(mag[i]), ALPHA_CAP);
+          al[j][i] = __uint_as_float(__float_as_uint(al_) | ((u ^ sp) & 0x80000000u));
+        }
       }
+      // running total in increasing edge order (bp.py:179-181)
+#pragma unroll
+      for (int j = 0; j < DV; ++j)
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
     }
-    // running total in increasing edge order (bp.py:179-181)
-#pragma unroll
-    for (int j = 0; j < DV; ++j)
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) tot[i] = __fadd_rn(tot[i], al[j][i]);
   }
   const unsigned lanes = es.lanes;
   if constexpr (!(FLAGS & AGG_LAST)) {
@@ -561,7 +591,15 @@ int agg_mode() {
 constexpr int AGG_LANE_GROUP = 128;   // lanes per lane group (check-record L2 working set)
 constexpr int AGG_REVERSE = 1;        // variable job visits lane groups last-to-first
 constexpr int AGG_VV = 4;             // lanes per thread of the standalone variable job
-constexpr int AGG_ITEMS = 2;          // rows per variable thread (L2 prefetch of the second, +1.5%)
+#ifndef AGG_ITEMS_N
+#define AGG_ITEMS_N 1
+#endif
+// rows per variable thread: with one-field record gathers, 1 row (no
+// loop-carried state, no spills) is as fast as 2 rows with an L2 prefetch of the
+// second on the fixed decode and 15% faster on the early-stop one
+// (profiles/r02/kbench_items_minb.md)
+constexpr int AGG_ITEMS = AGG_ITEMS_N;
+
 constexpr int AGG_FVC = 4;            // lanes per thread of the fused check job (+2.4% over 2)
 
 bool dc_supported(int dc) { return dc == 4 || dc == 6 || dc == 8 || dc == 12 || dc == 16 || dc == 24 || dc == 32; }
@@ -739,7 +777,7 @@ bool agg_eligible(const qc_plan* p) {
 }
 
 size_t agg_words(const qc_plan* p, int gamma) {
-  return agg_eligible(p) ? (size_t)3 * p->M * (size_t)(gamma > 0 ? gamma : 0) : 0;
+  return agg_eligible(p) ? (size_t)AGG_FIELDS * p->M * (size_t)(gamma > 0 ? gamma : 0) : 0;
 }
 
 int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, const float* mu, float* agg,

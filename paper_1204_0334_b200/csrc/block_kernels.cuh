@@ -94,8 +94,9 @@ __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned 
       }
     }
   }
-  // S2 excludes the first maximum; an exactly tied maximum has the same
-  // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
+  // S2 excludes the first maximum.  An edge holding more than half of S is
+  // the unique maximum and takes S2; every other edge takes S - psi_k >= S/2
+  // (no cancellation).  The compact schedule (agg.cu) applies the same rule.
   if constexpr (VEC % 2 == 0) {
     // lane pairs on the packed fp32 pipe (bit-identical to the scalar form)
 #pragma unroll
@@ -108,7 +109,7 @@ __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned 
           float d0, d1;
           get2(sub2(mk2(S[i], S[i + 1]), mk2(f0, f1)), d0, d1);
           float p0, p1;
-          get2(phi_of_log2_g2<REL>(mk2((f0 == mx[i]) ? S2[i] : d0, (f1 == mx[i + 1]) ? S2[i + 1] : d1)), p0, p1);
+          get2(phi_of_log2_g2<REL>(mk2((f0 > d0) ? S2[i] : d0, (f1 > d1) ? S2[i + 1] : d1)), p0, p1);
           if ((lanes >> i) & 1u)
             x[k][i] = __uint_as_float(__float_as_uint(fminf(p0, ALPHA_CAP)) | ((u0 ^ par[i]) & 0x80000000u));
           if ((lanes >> (i + 1)) & 1u)
@@ -125,7 +126,8 @@ __device__ __forceinline__ void cnu_core(float (&x)[DC][VEC], int deg, unsigned 
         if (k < deg) {
           unsigned u = __float_as_uint(x[k][i]);
           float f = __uint_as_float(u & 0x7fffffffu);
-          float mag = (f == mx[i]) ? S2[i] : __fsub_rn(S[i], f);
+          const float d = __fsub_rn(S[i], f);
+          float mag = (f > d) ? S2[i] : d;
           float a = fminf(phi_of_log2_g<REL>(mag), ALPHA_CAP);
           x[k][i] = __uint_as_float(__float_as_uint(a) | ((u ^ par[i]) & 0x80000000u));
         }

@@ -165,9 +165,10 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
       if ((present >> k) & 1ull) {
         unsigned u = __float_as_uint(x[k][i]);
         float f = __uint_as_float(u & 0x7fffffffu);
-        // S2 excludes the first maximum; an exactly tied maximum has the same
-        // exclusive sum (S - mx == S2), so every edge equal to mx takes S2
-        float mag = (f == mx) ? S2 : __fsub_rn(S, f);
+        // S2 excludes the first maximum: the dominant edge (more than half of
+        // S, necessarily the maximum) takes it, every other edge S - psi_k
+        const float d = __fsub_rn(S, f);
+        float mag = (f > d) ? S2 : d;
         float al = fminf(phi_of_log2_rel(mag), ALPHA_CAP);
         x[k][i] = __uint_as_float(__float_as_uint(al) | ((u ^ par) & 0x80000000u));
       }
