@@ -236,6 +236,16 @@ QC_API int cc_plan_dims(const cc_plan* plan, int64_t* dims);
  * counter, so a CUDA graph of K slots can be replayed; see cc_advance). */
 QC_API int cc_slot(const cc_plan* plan, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg,
             float* ring, const float* mu_in, float* post_out, int32_t* lane_cnt, void* stream);
+/* Part of slot t: parts bit 0 = entry of frame t, bit 1 = check phase, bit 2 =
+ * variable phase, of processors [ip0, ip0 + nip) only (0-based; processor I-1
+ * emits).  Within a slot the processors' (check, variable) pairs and the entry
+ * touch disjoint edges and ring slots, so the emitting processor can run
+ * first and the rest after it -- StreamDecoder.push_frame returns the emitted
+ * frame while the other I-1 processors and the next frame's copy-in proceed.
+ * cc_slot = cc_slot_part(..., 0, I, 7, ...). */
+QC_API int cc_slot_part(const cc_plan* plan, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg,
+                        float* ring, const float* mu_in, float* post_out, int32_t* lane_cnt, int ip0, int nip,
+                        int parts, void* stream);
 /* fold the last emitted frame's count into lane_cnt rows 1-2 (end of segment) */
 QC_API int cc_fold(int32_t* lane_cnt, int gamma, void* stream);
 /* *t_dev += k (ends a graph of k slots). */

@@ -71,6 +71,7 @@ SIGNATURES = {
     "cc_plan_destroy": (None, [_p]),
     "cc_plan_dims": (_i, [_p, _p]),
     "cc_slot": (_i, [_p, _i, _i, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "cc_slot_part": (_i, [_p, _i, _i, _i64, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p]),
     "cc_advance": (_i, [_p, _i64, _p]),
     "cc_fold": (_i, [_p, _i, _p]),
     "cc_channel": (_i, [_p, _u64, _u64, _u64, _p, _i64, _p, _i, _d, _p, _p]),

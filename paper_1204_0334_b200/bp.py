@@ -432,9 +432,16 @@ def host_array(a: np.ndarray) -> np.ndarray:
 def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool,
                   pinned_input: bool = False) -> HostDecoder:
     import torch
-    # small batches: chunk rounded up to a multiple of 64 lanes (<= 8 distinct
-    # decoders below HOST_CHUNK; each holds device buffers and captured graphs)
-    chunk = min(HOST_CHUNK, pad32(gamma) if gamma <= 32 else (gamma + 63) // 64 * 64)
+    # small batches: one chunk rounded up to a multiple of 64 lanes; from 256
+    # lanes up at least two chunks, so the copy-in of one overlaps the decode of
+    # another (e.g. 512 lanes: 64 + 128 + 256 + 64 over chunk 256, 1.6x the
+    # single-chunk rate; profiles/r02/e2e_gamma_curve.md)
+    if gamma <= 32:
+        chunk = pad32(gamma)
+    elif gamma < 256:
+        chunk = (gamma + 63) // 64 * 64
+    else:
+        chunk = min(HOST_CHUNK, max(128, ((gamma + 1) // 2 + 63) // 64 * 64))
     slots = (HOST_SLOTS_PINNED if pinned_input else HOST_SLOTS) if gamma > chunk else 1
     cache = layout.__dict__.setdefault("_host_decoders", {})
     key = (chunk, slots, iterations, bool(early_stop), torch.cuda.current_device())

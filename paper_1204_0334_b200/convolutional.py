@@ -117,6 +117,10 @@ class StreamDecoder:
         self._mu = torch.empty((code.c, self._gp), dtype=torch.float32, device=dev)
         self._post = torch.zeros((code.c, self._gp), dtype=torch.float32, device=dev)
         self._y = torch.empty((gamma, code.c), dtype=torch.float64, device=dev)
+        self._y_host = None      # page-locked staging of pushed frames
+        self._lm = None          # lane-major device outputs of emitted frames
+        self._es = None          # side stream of the emitting processor (I >= 2)
+        self._ev_rest = None     # end of the last slot's main-stream work
         self._kind = np.zeros((processors, code.lam * code.lam), dtype=np.int8)
         self._ring_live = np.zeros(self.window, dtype=bool)
 
@@ -154,6 +158,8 @@ class StreamDecoder:
     def channel_memory(self) -> np.ndarray:
         """Channel LLR ring, (I*(m_s+1), c, gamma) float64 host copy; slots of
         emitted frames read 0.0 as in the reference (convolutional.py:331)."""
+        import torch
+        torch.cuda.synchronize()
         ring = self._ring[:, :, : self.gamma].double().cpu().numpy()
         ring[~self._ring_live] = 0.0
         return ring
@@ -165,6 +171,8 @@ class StreamDecoder:
         check->variable blocks, beta on variable->check blocks (converted from
         the device's phi form, beta = sign * phi(|psi| ln 2), within fp32
         rounding), 0.0 on never-written / emitted blocks."""
+        import torch
+        torch.cuda.synchronize()
         code = self.code
         m = self._msg[:, : self.gamma].double().cpu().numpy()
         m = m.reshape(self.processors, code.edge_count, self.gamma)
@@ -183,18 +191,35 @@ class StreamDecoder:
         return m
 
     def push_frame(self, y_frame: np.ndarray, sigma: float) -> DecodedFrame | None:
-        """Feed one received frame (gamma, c); return the emitted frame or None."""
+        """Feed one received frame (gamma, c); return the emitted frame or None.
+
+        The frame emitted at slot t (t - I*T + 1) does not depend on frame t for
+        I >= 2: the emitting processor's check and variable updates touch edges
+        and ring slots disjoint from the entry of frame t and from the other
+        processors' work (cc_slot_part).  So it runs first, on a side stream,
+        and its copy-out overlaps the host staging of frame t, its copy-in and
+        the other I - 1 processors, which keep running after this returns."""
         if self._flushed:
             raise RuntimeError("decoder already flushed; create a new one")
         y = np.atleast_2d(np.asarray(y_frame, dtype=np.float64))
         if y.shape != (self.gamma, self.code.c):
             raise ValueError(f"expected frame shape {(self.gamma, self.code.c)}, got {y.shape}")
         import torch
-        self._y.copy_(torch.from_numpy(np.ascontiguousarray(y)))
+        em = self._emit_begin()
+        # page-locked staging: the host copy and an asynchronous H2D
+        if self._y_host is None:
+            self._y_host = torch.empty((self.gamma, self.code.c), dtype=torch.float64, pin_memory=True)
+            self._y_ev = torch.cuda.Event()
+        else:
+            self._y_ev.synchronize()     # the previous frame's copy has left the staging buffer
+        self._y_host.copy_(torch.from_numpy(np.ascontiguousarray(y)))
+        self._y.copy_(self._y_host, non_blocking=True)
+        self._y_ev.record()
         s = abs(float(sigma))
         _lib.call("qc_llr_from_lane_major", self.code.c, self._gp, self.gamma, self._y.data_ptr(),
                   s if s > 0.0 else 1e-300, self._mu.data_ptr(), _lib.stream_handle())
-        return self._advance(self._mu, tail=False)
+        self._rest(self._mu, em is not None)
+        return self._emit_end(em, tail=False)
 
     def push_llr_device(self, mu_dev) -> DecodedFrame | None:
         """B200 extension: push a frame of LLRs already on the device, (c, gamma_pad) fp32."""
@@ -221,20 +246,83 @@ class StreamDecoder:
         return out
 
     def _advance(self, mu_dev, tail: bool) -> DecodedFrame | None:
+        em = self._emit_begin()
+        self._rest(mu_dev, em is not None)
+        return self._emit_end(em, tail)
+
+    def _emit_begin(self):
+        """Queue slot t's emitting processor (0-based I-1) on the side stream, then
+        the lane-major conversion and the copy-out of the emitted frame."""
         t = self.t
         j = t - self.window + 1
-        self._track(t)
-        _lib.call("cc_slot", self._plan.handle, self.processors, self._gp, t, None,
-                  self._msg.data_ptr(), self._ring.data_ptr(), _lib.ptr(mu_dev),
-                  self._post.data_ptr() if j >= 0 else None, None, _lib.stream_handle())
-        self.t = t + 1
-        if j < 0:
+        if j < 0 or self.processors < 2:
             return None
         import torch
+        from .bp import host_empty
+        if self._es is None:
+            self._es = torch.cuda.Stream()
+            self._lm = (torch.empty((self.gamma, self.code.c), dtype=torch.float64, device=self._post.device),
+                        torch.empty((self.gamma, self.code.c), dtype=torch.uint8, device=self._post.device))
+        es = self._es
+        if self._ev_rest is not None:
+            es.wait_event(self._ev_rest)          # slot t-1 complete
+        else:
+            es.wait_stream(torch.cuda.current_stream())
+        c, I = self.code.c, self.processors
+        _lib.call("cc_slot_part", self._plan.handle, I, self._gp, t, None, self._msg.data_ptr(),
+                  self._ring.data_ptr(), None, self._post.data_ptr(), None, I - 1, 1, 6, es.cuda_stream)
+        post_d, bits_d = self._lm
+        _lib.call("qc_lane_major", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
+                  bits_d.data_ptr(), es.cuda_stream)
+        post = host_empty((self.gamma, c), np.float64)
+        bits = host_empty((self.gamma, c), np.uint8)
+        with torch.cuda.stream(es):
+            torch.from_numpy(post).copy_(post_d, non_blocking=True)
+            torch.from_numpy(bits).copy_(bits_d, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        return j, post, bits, ev
+
+    def _rest(self, mu_dev, split: bool):
+        """Queue the rest of slot t on the main stream: the entry of frame t and
+        processors 0..I-2 (the whole slot when nothing was split off)."""
+        import torch
+        t = self.t
+        self._track(t)
+        I = self.processors
+        j = t - self.window + 1
+        post = self._post.data_ptr() if (j >= 0 and not split) else None
+        _lib.call("cc_slot_part", self._plan.handle, I, self._gp, t, None, self._msg.data_ptr(),
+                  self._ring.data_ptr(), _lib.ptr(mu_dev), post, None, 0, I - 1 if split else I, 7,
+                  _lib.stream_handle())
+        if self._ev_rest is None:
+            self._ev_rest = torch.cuda.Event()
+        self._ev_rest.record()
+        self.t = t + 1
+
+    def _emit_end(self, em, tail: bool) -> DecodedFrame | None:
+        j = self.t - self.window                  # the frame slot t (= self.t - 1) emits
+        if em is None:
+            if j < 0:
+                return None
+            return self._emit_sync(j, tail)       # I = 1: emitted by the whole slot on the main stream
+        jj, post, bits, ev = em
+        ev.synchronize()
+        return DecodedFrame(frame_index=jj, hard_bits=bits, posteriors=post, tail=tail)
+
+    def _emit_sync(self, j: int, tail: bool) -> DecodedFrame:
+        import torch
+        from .bp import host_empty
         c = self.code.c
-        post_d = torch.empty((self.gamma, c), dtype=torch.float64, device=self._post.device)
-        bits_d = torch.empty((self.gamma, c), dtype=torch.uint8, device=self._post.device)
+        if self._lm is None:
+            self._lm = (torch.empty((self.gamma, c), dtype=torch.float64, device=self._post.device),
+                        torch.empty((self.gamma, c), dtype=torch.uint8, device=self._post.device))
+        post_d, bits_d = self._lm
         _lib.call("qc_lane_major", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
                   bits_d.data_ptr(), _lib.stream_handle())
-        return DecodedFrame(frame_index=j, hard_bits=bits_d.cpu().numpy(),
-                            posteriors=post_d.cpu().numpy(), tail=tail)
+        post = host_empty((self.gamma, c), np.float64)
+        bits = host_empty((self.gamma, c), np.uint8)
+        torch.from_numpy(post).copy_(post_d, non_blocking=True)
+        torch.from_numpy(bits).copy_(bits_d, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return DecodedFrame(frame_index=j, hard_bits=bits, posteriors=post, tail=tail)

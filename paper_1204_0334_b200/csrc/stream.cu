@@ -74,6 +74,7 @@ struct SlotArgs {
   const int32_t* var_tab;
   const int64_t* t_dev;
   int t;                    // slot (t_dev: offset added to *t_dev); < 2^31
+  int ip0, nip;             // processors [ip0, ip0 + nip) of this launch (0-based; nip = I: the whole slot)
 };
 
 __device__ __forceinline__ int slot_of(const SlotArgs& a) {
@@ -224,9 +225,10 @@ __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __g
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)P.I * P.cb * GV) return;
-  int ip = (int)(tid / ((long long)P.cb * GV));
-  int rem = (int)(tid - (long long)ip * P.cb * GV);
+  if (tid >= (long long)a.nip * P.cb * GV) return;
+  const int ipl = (int)(tid / ((long long)P.cb * GV));
+  const int ip = a.ip0 + ipl;
+  int rem = (int)(tid - (long long)ipl * P.cb * GV);
   int r = rem / GV, q = rem - r * GV;
   const int s = t - ip * T;
   if (s < 0) return;
@@ -318,9 +320,10 @@ __global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __gri
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)P.I * P.c * GV) return;
-  int ip = (int)(tid / ((long long)P.c * GV));
-  int rem = (int)(tid - (long long)ip * P.c * GV);
+  if (tid >= (long long)a.nip * P.c * GV) return;
+  const int ipl = (int)(tid / ((long long)P.c * GV));
+  const int ip = a.ip0 + ipl;
+  int rem = (int)(tid - (long long)ipl * P.c * GV);
   int v = rem / GV, q = rem - v * GV;
   const int j = t - (ip + 1) * T + 1;
   if (j < 0) return;
@@ -422,53 +425,65 @@ void launch_entry(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
 template <int DC, bool QC, int TT = 0, int WW = 0>
 void launch_check(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, DC > 24 ? 1 : 2);
-  long long n = (long long)P.I * P.cb * (P.gamma / vec);
+  long long n = (long long)a.nip * P.cb * (P.gamma / vec);
   if (vec == 2) launch_pdl(check_kernel<DC, 2, QC, TT, WW>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
   else launch_pdl(check_kernel<DC, 1, QC, TT, WW>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
 }
 template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_var(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
   int vec = vec_for(P.gamma, 4);
-  long long n = (long long)P.I * P.c * (P.gamma / vec);
+  long long n = (long long)a.nip * P.c * (P.gamma / vec);
   if (vec == 4) launch_pdl(var_kernel<DV, 4, QC, TT, SJ>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
   else if (vec == 2) launch_pdl(var_kernel<DV, 2, QC, TT, SJ>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
   else launch_pdl(var_kernel<DV, 1, QC, TT, SJ>, dim3(blocks_for(n, CC_THREADS)), CC_THREADS, s, a, P);
 }
 
+// parts: bit 0 = entry, bit 1 = check phase, bit 2 = variable phase (of the
+// processors [a.ip0, a.ip0 + a.nip))
+enum { SLOT_ENTRY = 1, SLOT_CHECK = 2, SLOT_VAR = 4, SLOT_ALL = 7 };
+
 template <int DV, bool QC>
-int launch_slot_dv(const CcParams& P, const SlotArgs& a, int dc, cudaStream_t s) {
+int launch_slot_dv(const CcParams& P, const SlotArgs& a, int dc, int parts, cudaStream_t s) {
   if constexpr (QC && DV == 4) {   // compile-time walks for the common unwrapped shapes
     if (P.lam == 4 && P.sj == 1 && P.sl == 6) {          // (4, 24) grids: codes A', 18360'
-      launch_entry<4, true, 4, 1>(P, a, s); launch_check<24, true, 4, 6>(P, a, s); launch_var<4, true, 4, 1>(P, a, s);
+      if (parts & SLOT_ENTRY) launch_entry<4, true, 4, 1>(P, a, s);
+      if (parts & SLOT_CHECK) launch_check<24, true, 4, 6>(P, a, s);
+      if (parts & SLOT_VAR) launch_var<4, true, 4, 1>(P, a, s);
       return 0;
     }
     if (P.lam == 4 && P.sj == 1 && P.sl == 2) {          // (4, 8) grids
-      launch_entry<4, true, 4, 1>(P, a, s); launch_check<8, true, 4, 2>(P, a, s); launch_var<4, true, 4, 1>(P, a, s);
+      if (parts & SLOT_ENTRY) launch_entry<4, true, 4, 1>(P, a, s);
+      if (parts & SLOT_CHECK) launch_check<8, true, 4, 2>(P, a, s);
+      if (parts & SLOT_VAR) launch_var<4, true, 4, 1>(P, a, s);
       return 0;
     }
   }
   if constexpr (QC && DV == 2) {
     if (P.lam == 2 && P.sj == 1 && P.sl == 2) {          // (2, 4) grids
-      launch_entry<2, true, 2, 1>(P, a, s); launch_check<4, true, 2, 2>(P, a, s); launch_var<2, true, 2, 1>(P, a, s);
+      if (parts & SLOT_ENTRY) launch_entry<2, true, 2, 1>(P, a, s);
+      if (parts & SLOT_CHECK) launch_check<4, true, 2, 2>(P, a, s);
+      if (parts & SLOT_VAR) launch_var<2, true, 2, 1>(P, a, s);
       return 0;
     }
   }
-  launch_entry<DV, QC>(P, a, s);
-  if (dc <= 4) launch_check<4, QC>(P, a, s);
-  else if (dc <= 8) launch_check<8, QC>(P, a, s);
-  else if (dc <= 16) launch_check<16, QC>(P, a, s);
-  else if (dc <= 24) launch_check<24, QC>(P, a, s);
-  else if (dc <= 32) launch_check<32, QC>(P, a, s);
-  else return fail_arg("LDPCCC check degree > 32 is not supported");
-  launch_var<DV, QC>(P, a, s);
+  if (parts & SLOT_ENTRY) launch_entry<DV, QC>(P, a, s);
+  if (parts & SLOT_CHECK) {
+    if (dc <= 4) launch_check<4, QC>(P, a, s);
+    else if (dc <= 8) launch_check<8, QC>(P, a, s);
+    else if (dc <= 16) launch_check<16, QC>(P, a, s);
+    else if (dc <= 24) launch_check<24, QC>(P, a, s);
+    else if (dc <= 32) launch_check<32, QC>(P, a, s);
+    else return fail_arg("LDPCCC check degree > 32 is not supported");
+  }
+  if (parts & SLOT_VAR) launch_var<DV, QC>(P, a, s);
   return 0;
 }
 
 template <bool QC>
-int launch_slot(const CcParams& P, const SlotArgs& a, int dc, int dv, cudaStream_t s) {
-  if (dv <= 2) return launch_slot_dv<2, QC>(P, a, dc, s);
-  if (dv <= 4) return launch_slot_dv<4, QC>(P, a, dc, s);
-  if (dv <= 8) return launch_slot_dv<8, QC>(P, a, dc, s);
+int launch_slot(const CcParams& P, const SlotArgs& a, int dc, int dv, int parts, cudaStream_t s) {
+  if (dv <= 2) return launch_slot_dv<2, QC>(P, a, dc, parts, s);
+  if (dv <= 4) return launch_slot_dv<4, QC>(P, a, dc, parts, s);
+  if (dv <= 8) return launch_slot_dv<8, QC>(P, a, dc, parts, s);
   return fail_arg("LDPCCC variable degree > 8 is not supported");
 }
 
@@ -568,22 +583,32 @@ int cc_plan_dims(const cc_plan* pl, int64_t* dims) {
   return 0;
 }
 
-int cc_slot(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg, float* ring,
-            const float* mu_in, float* post_out, int32_t* lane_cnt, void* stream) {
+int cc_slot_part(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg, float* ring,
+                 const float* mu_in, float* post_out, int32_t* lane_cnt, int ip0, int nip, int parts,
+                 void* stream) {
   if (!pl || !msg || !ring) return fail_arg("null argument");
   if (I < 1) return fail_arg("need at least one processor");
   if (gamma <= 0 || gamma % 32) return fail_arg("gamma must be a positive multiple of 32");
   if (!t_dev && t < 0) return fail_arg("slot index must be non-negative");
   if (t > 0x3fffffff || t < -0x3fffffff) return fail_arg("slot index out of range");
+  if (ip0 < 0 || nip < 0 || ip0 + nip > I || parts < 0 || parts > SLOT_ALL)
+    return fail_arg("processor range / parts out of range");
+  if (parts == 0 || (nip == 0 && !(parts & SLOT_ENTRY))) return 0;
   cudaStream_t s = as_stream(stream);
   CcParams P = make_params(pl, I, gamma);
-  SlotArgs a{msg, ring, mu_in, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t};
+  SlotArgs a{msg, ring, mu_in, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t, ip0, nip};
+  if (nip == 0) parts &= SLOT_ENTRY;
   const bool qc = pl->all_live;
   const int dc = pl->lam * (qc ? pl->sl : pl->wmax);
   const int dv = pl->lam * pl->sj;
-  int rc = qc ? launch_slot<true>(P, a, dc, dv, s) : launch_slot<false>(P, a, dc, dv, s);
+  int rc = qc ? launch_slot<true>(P, a, dc, dv, parts, s) : launch_slot<false>(P, a, dc, dv, parts, s);
   if (rc) return rc;
   return check_launch("cc_slot");
+}
+
+int cc_slot(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg, float* ring,
+            const float* mu_in, float* post_out, int32_t* lane_cnt, void* stream) {
+  return cc_slot_part(pl, I, gamma, t, t_dev, msg, ring, mu_in, post_out, lane_cnt, 0, I, SLOT_ALL, stream);
 }
 
 int cc_fold(int32_t* lane_cnt, int gamma, void* stream) {
