@@ -18,7 +18,8 @@ the same with y in ordinary pageable memory.
 
 `roofline` = the dominant launch, the fused half-iteration kernel of the
 compact check-state schedule: its compulsory bytes per
-launch (4 (3E + N + 6M) per lane of the half) / its CUDA-event-timed duration,
+launch (4 (3E + N + 3M) per lane of the half: 2-field check records, one
+field gathered by the variable job) / its CUDA-event-timed duration,
 against the measured HBM copy bandwidth in MEASURED_PEAKS.json;
 `ref_schedule` restates the same time in the reference schedule's bytes
 (4 (4E + N) per lane-iteration), which the compact schedule beats.
@@ -420,18 +421,20 @@ def main():
     fused_ms, check_ms = ev_ms(fused), ev_ms(check)
     peak, peak_kind = load_peaks()
     # compulsory bytes of the compact schedule, per lane and iteration:
-    # check job reads E packages, writes 3M record words; variable job reads E
-    # packages + N LLRs + 3M record words once, writes E packages
-    fused_bytes = 4 * (3 * E + N + 6 * M) * H
+    # check job reads E packages, writes 2M record words (S|par, S2); variable
+    # job reads E packages + N LLRs + the M S|par words once (the S2 reads of
+    # dominant edges, a few % of edge-vectors, are data-dependent and not
+    # counted), writes E packages
+    fused_bytes = 4 * (3 * E + N + 3 * M) * H
     ref_bytes = 4 * (4 * E + N) * H             # the reference schedule's bytes for the same work
-    check_bytes = 4 * (E + 3 * M) * gamma
+    check_bytes = 4 * (E + 2 * M) * gamma
     fach = fused_bytes / (fused_ms / 1e3) / 1e9
     step_alg = algorithmic_bytes_per_codeword(E, N, ITERS) * gamma
     tf = ncu_traffic("agg_fused", gamma)
     roofline = {"bound": "hbm", "achieved": round(fach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(fach / peak, 4),
                 "traffic": int(tf["dram_bytes"]) if tf else None,
-                "kernel": "agg_fused_kernel<24,4,4,4,0,0,2> (variable job + check job, compact schedule; "
+                "kernel": "agg_fused_kernel<24,4,4,4,0,0,1> (variable job + check job, compact schedule; "
                           "59 of 65 launches of a 30-iteration decode)",
                 "peak_kind": peak_kind, "bytes_per_launch": fused_bytes, "launch_ms": round(fused_ms, 4),
                 "traffic_source": (tf or {}).get("source"),
@@ -445,8 +448,8 @@ def main():
                 "step": {"ref_schedule_alg_bytes": step_alg,
                          "ref_schedule_equiv_GBs": round(step_alg / (ms / args.steps / 1e3) / 1e9, 1),
                          "ref_schedule_equiv_frac": round(step_alg / (ms / args.steps / 1e3) / 1e9 / peak, 4),
-                         "compact_alg_bytes": 4 * ITERS * (3 * E + N + 6 * M) * gamma,
-                         "compact_frac": round(4 * ITERS * (3 * E + N + 6 * M) * gamma /
+                         "compact_alg_bytes": 4 * ITERS * (3 * E + N + 3 * M) * gamma,
+                         "compact_frac": round(4 * ITERS * (3 * E + N + 3 * M) * gamma /
                                                (ms / args.steps / 1e3) / 1e9 / peak, 4)}}
     del check
 
