@@ -246,6 +246,17 @@ QC_API int cc_slot(const cc_plan* plan, int I, int gamma, int64_t t, const int64
 QC_API int cc_slot_part(const cc_plan* plan, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg,
                         float* ring, const float* mu_in, float* post_out, int32_t* lane_cnt, int ip0, int nip,
                         int parts, void* stream);
+/* Look-ahead slot for device-resident campaigns (harness.py:226-232 with every
+ * frame's LLRs known up front): the check and variable phases of slot t, where
+ * the check phase folds the previous emission's count (the entry kernel's job
+ * in cc_slot) and, when enter_next != 0, the emitting processor's variable
+ * threads enter frame t + 1 from mu_next (NULL = zero-LLR virtual frame) right
+ * after emitting frame t + 1 - I(ms+1), which used the same ring slot and edge
+ * slots.  Two launches per slot instead of three; frame 0 is entered with
+ * cc_slot_part(parts = 1).  Results equal cc_slot bit for bit. */
+QC_API int cc_slot_ahead(const cc_plan* plan, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg,
+                         float* ring, const float* mu_next, int enter_next, float* post_out, int32_t* lane_cnt,
+                         void* stream);
 /* fold the last emitted frame's count into lane_cnt rows 1-2 (end of segment) */
 QC_API int cc_fold(int32_t* lane_cnt, int gamma, void* stream);
 /* *t_dev += k (ends a graph of k slots). */
@@ -255,6 +266,11 @@ QC_API int cc_advance(int64_t* t_dev, int64_t k, void* stream);
 QC_API int cc_channel(const cc_plan* plan, uint64_t seed_lo, uint64_t seed_hi, uint64_t lane0,
                       const uint64_t* lane0_dev, int64_t t, const int64_t* t_dev, int gamma,
                       double sigma, float* mu, void* stream);
+/* Frames t .. t + nframes - 1 in one launch (contiguous positions t*c ..), into
+ * mu (nframes, c, gamma): amortises the channel over several slots. */
+QC_API int cc_channel_frames(const cc_plan* plan, uint64_t seed_lo, uint64_t seed_hi, uint64_t lane0,
+                             const uint64_t* lane0_dev, int64_t t, int nframes, int gamma, double sigma,
+                             float* mu, void* stream);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,8 @@ SIGNATURES = {
     "cc_advance": (_i, [_p, _i64, _p]),
     "cc_fold": (_i, [_p, _i, _p]),
     "cc_channel": (_i, [_p, _u64, _u64, _u64, _p, _i64, _p, _i, _d, _p, _p]),
+    "cc_channel_frames": (_i, [_p, _u64, _u64, _u64, _p, _i64, _i, _i, _d, _p, _p]),
+    "cc_slot_ahead": (_i, [_p, _i, _i, _i64, _p, _p, _p, _p, _i, _p, _p, _p]),
 }
 
 _LIB = None

@@ -75,6 +75,12 @@ struct SlotArgs {
   const int64_t* t_dev;
   int t;                    // slot (t_dev: offset added to *t_dev); < 2^31
   int ip0, nip;             // processors [ip0, ip0 + nip) of this launch (0-based; nip = I: the whole slot)
+  // look-ahead slot form (cc_slot_ahead): the check phase folds the previous
+  // emission's counters, and the emitting processor's variable threads enter
+  // frame t + 1 (mu_next; null = zero-LLR virtual frame) right after emitting
+  // frame t + 1 - window, which held the same ring slot and edge slots
+  const float* mu_next;
+  int fold_in_check, entry_next;
 };
 
 __device__ __forceinline__ int slot_of(const SlotArgs& a) {
@@ -177,42 +183,54 @@ __device__ __forceinline__ void cnu_core_mask(float (&x)[DC][VEC], unsigned long
   }
 }
 
-// ---- entry: frame t into ring slot t mod window and its T sub-blocks --------
-// Also folds the previous slot's emitted-frame bit count into the lane counters.
+// ---- entry: frame tf into ring slot tf mod window and its T sub-blocks -----
 template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
-__global__ void __launch_bounds__(CC_THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
-  pdl_trigger();
-  pdl_wait();
-  const int t = slot_of(a);
-  const int T = TT ? TT : P.lam, GV = P.gamma / VEC, window = P.I * T;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (a.cnt && t >= window && tid < P.gamma) {   // previous slot emitted a frame
-    int g = (int)tid;
-    int b = a.cnt[g];
-    a.cnt[P.gamma + g] += b;
-    a.cnt[2 * P.gamma + g] += b > 0;
-    a.cnt[g] = 0;
-  }
-  if (tid >= (long long)P.c * GV) return;
-  int v = (int)(tid / GV), q = (int)(tid - (long long)v * GV);
+__device__ __forceinline__ void entry_body(const SlotArgs& a, const CcParams& P, int tf, const float* mu_src, int v,
+                                           int q) {
+  const int T = TT ? TT : P.lam, window = P.I * T;
   float m[VEC];
-  if (a.mu_in) vload<VEC>(a.mu_in + (size_t)v * P.gamma + q * VEC, m);
+  if (mu_src) vload<VEC>(mu_src + (size_t)v * P.gamma + q * VEC, m);
   else {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) m[i] = 0.0f;
   }
-  vstore<VEC>(a.ring + ((size_t)pmod(t, window) * P.c + v) * P.gamma + q * VEC, m);
+  vstore<VEC>(a.ring + ((size_t)pmod(tf, window) * P.c + v) * P.gamma + q * VEC, m);
   // beta^0 = mu into the frame's T sub-blocks, stored in phi form
 #pragma unroll
   for (int i = 0; i < VEC; ++i)
     m[i] = __uint_as_float(__float_as_uint(psi_of_nat(fabsf(m[i]))) | (__float_as_uint(m[i]) & 0x80000000u));
   const int bc = v / P.p, cc = v - bc * P.p;
   unsigned e[DV];
-  unsigned present = var_edges<DV, QC, TT, SJ>(P, a.var_tab, pmod(t, T), (unsigned)pmod(t / T, P.I) * (unsigned)P.E,
+  unsigned present = var_edges<DV, QC, TT, SJ>(P, a.var_tab, pmod(tf, T), (unsigned)pmod(tf / T, P.I) * (unsigned)P.E,
                                                 v, bc, cc, e);
 #pragma unroll
   for (int k = 0; k < DV; ++k)
     if ((present >> k) & 1u) vstore<VEC>(a.msg + (size_t)e[k] * P.gamma + q * VEC, m);
+}
+
+// fold the bit count of the frame the previous slot emitted into the lane counters
+__device__ __forceinline__ void fold_prev(const SlotArgs& a, const CcParams& P, int t, int window, long long tid) {
+  if (a.cnt && t >= window && tid < P.gamma) {
+    const int g = (int)tid;
+    const int b = a.cnt[g];
+    a.cnt[P.gamma + g] += b;
+    a.cnt[2 * P.gamma + g] += b > 0;
+    a.cnt[g] = 0;
+  }
+}
+
+// Also folds the previous slot's emitted-frame bit count into the lane counters.
+template <int DV, int VEC, bool QC, int TT = 0, int SJ = 0>
+__global__ void __launch_bounds__(CC_THREADS) entry_kernel(SlotArgs a, const __grid_constant__ CcParams P) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = slot_of(a);
+  const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
+  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  fold_prev(a, P, t, P.I * T, tid);
+  if (tid >= (long long)P.c * GV) return;
+  const int v = (int)(tid / GV), q = (int)(tid - (long long)v * GV);
+  entry_body<DV, VEC, QC, TT, SJ>(a, P, t, a.mu_in, v, q);
 }
 
 // ---- check phase: processors i = 1..I refresh layer s = t - (i-1)T ---------
@@ -225,6 +243,7 @@ __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __g
   const int t = slot_of(a);
   const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
   long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.fold_in_check) fold_prev(a, P, t, P.I * T, tid);
   if (tid >= (long long)a.nip * P.cb * GV) return;
   const int ipl = (int)(tid / ((long long)P.cb * GV));
   const int ip = a.ip0 + ipl;
@@ -326,7 +345,11 @@ __global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __gri
   int rem = (int)(tid - (long long)ipl * P.c * GV);
   int v = rem / GV, q = rem - v * GV;
   const int j = t - (ip + 1) * T + 1;
-  if (j < 0) return;
+  const bool enter = a.entry_next && ip + 1 == P.I;   // look-ahead entry of frame t + 1 (= j + window)
+  if (j < 0) {
+    if (enter) entry_body<DV, VEC, QC, TT, SJ>(a, P, t + 1, a.mu_next, v, q);
+    return;
+  }
   const int bc = v / P.p, cc = v - bc * P.p;
   unsigned e[DV];
   unsigned present = var_edges<DV, QC, TT, SJ>(P, a.var_tab, pmod(j, T), (unsigned)pmod(j / T, P.I) * (unsigned)P.E,
@@ -379,6 +402,7 @@ __global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __gri
       for (int i = 0; i < VEC; ++i)
         if (pst[i] < 0.0f) atomicAdd(a.cnt + q * VEC + i, 1);
     }
+    if (enter) entry_body<DV, VEC, QC, TT, SJ>(a, P, t + 1, a.mu_next, v, q);
   }
 }
 
@@ -596,7 +620,8 @@ int cc_slot_part(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* 
   if (parts == 0 || (nip == 0 && !(parts & SLOT_ENTRY))) return 0;
   cudaStream_t s = as_stream(stream);
   CcParams P = make_params(pl, I, gamma);
-  SlotArgs a{msg, ring, mu_in, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t, ip0, nip};
+  SlotArgs a{msg, ring, mu_in, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t, ip0, nip,
+             nullptr, 0, 0};
   if (nip == 0) parts &= SLOT_ENTRY;
   const bool qc = pl->all_live;
   const int dc = pl->lam * (qc ? pl->sl : pl->wmax);
@@ -609,6 +634,26 @@ int cc_slot_part(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* 
 int cc_slot(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg, float* ring,
             const float* mu_in, float* post_out, int32_t* lane_cnt, void* stream) {
   return cc_slot_part(pl, I, gamma, t, t_dev, msg, ring, mu_in, post_out, lane_cnt, 0, I, SLOT_ALL, stream);
+}
+
+int cc_slot_ahead(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* t_dev, float* msg, float* ring,
+                  const float* mu_next, int enter_next, float* post_out, int32_t* lane_cnt, void* stream) {
+  if (!pl || !msg || !ring) return fail_arg("null argument");
+  if (I < 1) return fail_arg("need at least one processor");
+  if (gamma <= 0 || gamma % 32) return fail_arg("gamma must be a positive multiple of 32");
+  if (!t_dev && t < 0) return fail_arg("slot index must be non-negative");
+  if (t > 0x3fffffff || t < -0x3fffffff) return fail_arg("slot index out of range");
+  cudaStream_t s = as_stream(stream);
+  CcParams P = make_params(pl, I, gamma);
+  SlotArgs a{msg, ring, nullptr, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t, 0, I,
+             mu_next, 1, enter_next ? 1 : 0};
+  const bool qc = pl->all_live;
+  const int dc = pl->lam * (qc ? pl->sl : pl->wmax);
+  const int dv = pl->lam * pl->sj;
+  const int parts = SLOT_CHECK | SLOT_VAR;
+  int rc = qc ? launch_slot<true>(P, a, dc, dv, parts, s) : launch_slot<false>(P, a, dc, dv, parts, s);
+  if (rc) return rc;
+  return check_launch("cc_slot_ahead");
 }
 
 int cc_fold(int32_t* lane_cnt, int gamma, void* stream) {
@@ -639,4 +684,16 @@ extern "C" int cc_channel(const cc_plan* pl, uint64_t seed_lo, uint64_t seed_hi,
   if (!t_dev && t < 0) return fail_arg("frame index must be non-negative");
   return launch_channel_t(seed_lo, seed_hi, lane0, lane0_dev, 0, t_dev, (long long)t, (long long)pl->c, pl->c,
                           gamma, sigma, mu, as_stream(stream));
+}
+
+extern "C" int cc_channel_frames(const cc_plan* pl, uint64_t seed_lo, uint64_t seed_hi, uint64_t lane0,
+                                 const uint64_t* lane0_dev, int64_t t, int nframes, int gamma, double sigma,
+                                 float* mu, void* stream) {
+  if (!pl || !mu) return fail_arg("null argument");
+  if (gamma <= 0 || gamma % 32) return fail_arg("gamma must be a positive multiple of 32");
+  if (t < 0 || nframes < 1) return fail_arg("frame range must be non-negative and non-empty");
+  if ((long long)nframes * pl->c > 0x7fffffffll) return fail_arg("too many frames for one channel launch");
+  // frames t .. t + nframes - 1 are the contiguous positions [t c, (t + nframes) c)
+  return launch_channel_t(seed_lo, seed_hi, lane0, lane0_dev, (uint64_t)t * (uint64_t)pl->c, nullptr, 0, 0,
+                          nframes * pl->c, gamma, sigma, mu, as_stream(stream));
 }

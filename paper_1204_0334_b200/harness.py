@@ -404,25 +404,48 @@ class StreamCampaign:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.msg = torch.zeros((processors * code.edge_count, self.gp), dtype=torch.float32, device=dev)
         self.ring = torch.zeros((self.window, code.c, self.gp), dtype=torch.float32, device=dev)
-        self.mu = torch.zeros((code.c, self.gp), dtype=torch.float32, device=dev)
+        # channel LLRs of K frames per launch (cc_channel_frames): one launch of
+        # ~8M normals fills the machine where a single small frame is latency-bound
+        # (running the batches on a side stream beside the slot kernels measured
+        # no faster, profiles/r02/sbench_lookahead.md)
+        self.K = max(1, min(pushes, 16, (8 << 20) // max(1, code.c * self.gp)))
+        self.mu = torch.zeros((self.K, code.c, self.gp), dtype=torch.float32, device=dev)
         self.cnt = torch.zeros((3, self.gp), dtype=torch.int32, device=dev)
         self.lane0 = torch.zeros(1, dtype=torch.int64, device=dev)
         self.sigma = None
         self._graph = None
         self._use_graph = graph
 
+    def _channel(self, b, s):
+        t = b * self.K
+        _lib.call("cc_channel_frames", self.plan.handle, self.k0, self.k1, 0, self.lane0.data_ptr(), t,
+                  min(self.K, self.pushes - t), self.gp, float(self.sigma), self.mu.data_ptr(), s)
+
+    def _frame(self, t):
+        return self.mu[t % self.K].data_ptr()
+
     def _launch(self):
+        # frame 0: channel batch + entry; then per slot t the look-ahead slot
+        # (check phase, variable phase entering frame t + 1: two launches) with
+        # the channel in batches of K frames -- the same results as
+        # channel + cc_slot per slot (tests/test_gpu_stream.py)
         s = _lib.stream_handle()
         self.cnt.zero_()
+        self._channel(0, s)
+        _lib.call("cc_slot_part", self.plan.handle, self.I, self.gp, 0, None, self.msg.data_ptr(),
+                  self.ring.data_ptr(), self._frame(0), None, self.cnt.data_ptr(), 0, 0, 1, s)
         for t in range(self.pushes):
-            _lib.call("cc_channel", self.plan.handle, self.k0, self.k1, 0, self.lane0.data_ptr(), t, None,
-                      self.gp, float(self.sigma), self.mu.data_ptr(), s)
-            _lib.call("cc_slot", self.plan.handle, self.I, self.gp, t, None, self.msg.data_ptr(),
-                      self.ring.data_ptr(), self.mu.data_ptr(), None, self.cnt.data_ptr(), s)
+            nxt = t + 1 < self.pushes
+            if nxt and (t + 1) % self.K == 0:
+                self._channel((t + 1) // self.K, s)     # after the slot that entered frame t (last of its batch)
+            _lib.call("cc_slot_ahead", self.plan.handle, self.I, self.gp, t, None, self.msg.data_ptr(),
+                      self.ring.data_ptr(), self._frame(t + 1) if nxt else None, int(nxt), None,
+                      self.cnt.data_ptr(), s)
         _lib.call("cc_fold", self.cnt.data_ptr(), self.gp, s)
 
     def kernel_launches_per_step(self) -> int:
-        return self.pushes * 4 + 1      # channel, entry(+fold), check, variable; final fold
+        # channel batches, entry of frame 0, (check, variable + next entry) per slot, final fold
+        return -(-self.pushes // self.K) + 1 + 2 * self.pushes + 1
 
     def step(self, lane0: int, sigma: float):
         import torch

@@ -143,3 +143,63 @@ def test_device_slot_counter_matches_host_slots(gpu):
         assert np.array_equal(a, b)
     # one emitted frame per slot from window-1 on, counters folded per frame
     assert int(outs[0][2][1].sum()) == int((outs[0][1][window - 1:] < 0).sum())
+
+
+@pytest.mark.parametrize("shape", ["qc_4x24", "zero_blocks", "n18360_prime"])
+def test_lookahead_slots_match_cc_slot(gpu, shape):
+    """cc_slot_ahead (check + variable phase, the emitting processor entering
+    frame t+1, the check phase folding counters) and cc_channel_frames (K frames
+    per launch) -- the StreamCampaign flow -- equal channel + cc_slot per slot
+    bit for bit: message store, ring, emitted posteriors, lane counters."""
+    import torch
+    from paper_1204_0334_b200 import _lib
+    q = gpu
+    if shape == "qc_4x24":
+        code, I, G = q.unwrap_qc(q.multiplicative_shifts(4, 24, 8)), 3, 64
+    elif shape == "zero_blocks":
+        sh = np.random.default_rng(9).integers(0, 11, size=(4, 8))
+        sh[0, 1] = sh[2, 5] = sh[3, 3] = -1
+        code, I, G = q.unwrap_qc(q.ExponentMatrix(sh, 11)), 2, 32
+    else:
+        _, exp = q.load_code(q.codes.bundled_code_path("n18360"))
+        code, I, G = q.unwrap_qc(exp), 2, 128
+    plan = code.plan()
+    window = I * (code.ms + 1)
+    P = window + 9                                   # pushes: bootstrap, steady state, emissions
+    sigma, k0, k1 = 0.9, 11, 3
+    lane0 = torch.tensor([5 * G], dtype=torch.int64, device="cuda")
+    outs = []
+    for mode in ("slot", "ahead"):
+        msg = torch.zeros((I * code.edge_count, G), dtype=torch.float32, device="cuda")
+        ring = torch.zeros((window, code.c, G), dtype=torch.float32, device="cuda")
+        post = torch.zeros((P, code.c, G), dtype=torch.float32, device="cuda")
+        cnt = torch.zeros((3, G), dtype=torch.int32, device="cuda")
+        s = _lib.stream_handle()
+        if mode == "slot":
+            mu = torch.zeros((code.c, G), dtype=torch.float32, device="cuda")
+            for t in range(P):
+                _lib.call("cc_channel", plan.handle, k0, k1, 0, lane0.data_ptr(), t, None, G, sigma,
+                          mu.data_ptr(), s)
+                _lib.call("cc_slot", plan.handle, I, G, t, None, msg.data_ptr(), ring.data_ptr(), mu.data_ptr(),
+                          post[t].data_ptr(), cnt.data_ptr(), s)
+        else:
+            K = 4
+            mu = torch.zeros((K, code.c, G), dtype=torch.float32, device="cuda")
+            frame = lambda t: mu[t % K].data_ptr()
+            _lib.call("cc_channel_frames", plan.handle, k0, k1, 0, lane0.data_ptr(), 0, K, G, sigma,
+                      mu.data_ptr(), s)
+            _lib.call("cc_slot_part", plan.handle, I, G, 0, None, msg.data_ptr(), ring.data_ptr(), frame(0),
+                      None, cnt.data_ptr(), 0, 0, 1, s)
+            for t in range(P):
+                nxt = t + 1 < P
+                if nxt and (t + 1) % K == 0:
+                    _lib.call("cc_channel_frames", plan.handle, k0, k1, 0, lane0.data_ptr(), t + 1,
+                              min(K, P - t - 1), G, sigma, mu.data_ptr(), s)
+                _lib.call("cc_slot_ahead", plan.handle, I, G, t, None, msg.data_ptr(), ring.data_ptr(),
+                          frame(t + 1) if nxt else None, int(nxt), post[t].data_ptr(), cnt.data_ptr(), s)
+        _lib.call("cc_fold", cnt.data_ptr(), G, s)
+        torch.cuda.synchronize()
+        outs.append((msg.cpu().numpy(), ring.cpu().numpy(), post[window - 1:].cpu().numpy(), cnt.cpu().numpy()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert int(outs[0][3][1].sum()) > 0 or float(np.abs(outs[0][2]).sum()) > 0

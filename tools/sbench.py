@@ -47,7 +47,7 @@ def main():
     slot = 4 * (4 * args.I * code.edge_count // code.lam + (args.I + 1) * code.c)
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
     gbs = slot * G * pushes / (ms / 1e3) / 1e9
-    print(json.dumps({"code": args.code, "I": args.I, "gamma": G, "pushes": pushes, "ms_per_segment": round(ms, 3),
+    print(json.dumps({"K": eng.K, "code": args.code, "I": args.I, "gamma": G, "pushes": pushes, "ms_per_segment": round(ms, 3),
                       "us_per_slot": round(ms * 1e3 / pushes, 2), "alg_gbs": round(gbs, 1),
                       "frac": round(gbs / peak, 4),
                       "mbit_s": round(counted * G * (code.c - code.cb) / (ms / 1e3) / 1e6, 1),
