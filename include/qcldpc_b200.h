@@ -120,6 +120,18 @@ QC_API int qc_agg_fused(const qc_plan* plan, int gamma, int lanes, int var_lane0
                         float* post, uint32_t* hb, void* stream);
 /* kernels qc_decode launches for these arguments (bench accounting) */
 QC_API int qc_decode_launches(const qc_plan* plan, int gamma, int iters, int early_stop);
+/* decode_llr_batch(..., early_stop=True) with lane compaction (bp.py:242-256):
+ * at a few checkpoint iterations the lanes still iterating are packed into a
+ * second buffer set, so converged lanes stop costing work; results equal
+ * qc_decode(early_stop = 1) bit for bit (posteriors, bits, ok, iterations_run).
+ * scratch: qc_decode_es_scratch_words(plan, gamma) 32-bit words of device
+ * memory (0 = plan / gamma / iterations not eligible: falls back to qc_decode).
+ * Other arguments as qc_decode. */
+QC_API int qc_decode_es(const qc_plan* plan, int gamma, int iters, const float* mu, float* msgs, float* post,
+                        uint32_t* hb, uint32_t* work, uint32_t* scratch, uint8_t* ok, int32_t* iters_run,
+                        int32_t* lane_bits, void* stream);
+QC_API size_t qc_decode_es_scratch_words(const qc_plan* plan, int gamma);
+QC_API int qc_decode_es_launches(const qc_plan* plan, int gamma, int iters);
 
 /* lane-major outputs (DecodeResult / DecodedFrame layout, bp.py:87-100,
  * convolutional.py:166-177): post (n, gamma) fp32 -> post_out (gamma_out, n)

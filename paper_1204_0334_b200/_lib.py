@@ -40,6 +40,9 @@ SIGNATURES = {
     "qc_decode_work_words": (C.c_size_t, [_p, _i]),
     "qc_decode_records_offset": (C.c_size_t, [_i]),
     "qc_decode": (_i, [_p, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "qc_decode_es": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "qc_decode_es_scratch_words": (C.c_size_t, [_p, _i]),
+    "qc_decode_es_launches": (_i, [_p, _i, _i]),
     "qc_agg_check": (_i, [_p, _i, _i, _p, _p, _p, _p]),
     "qc_agg_var": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p]),
     "qc_agg_fused": (_i, [_p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p]),

@@ -202,7 +202,7 @@ class BlockDecoder:
 
     def __init__(self, layout: EdgeLayout, gamma: int, iterations: int = 30,
                  early_stop: bool = False, graph: bool = True, count_bits: bool = True,
-                 precision: str | None = None):
+                 precision: str | None = None, compact: bool = True):
         torch = require_cuda()
         if iterations < 1:
             raise ValueError("need at least one iteration")
@@ -220,6 +220,10 @@ class BlockDecoder:
         self.post = torch.zeros((N, gp), dtype=f32, device=dev)
         self.hb = torch.zeros((N, gp // 32), dtype=i32, device=dev)
         self.work = torch.zeros(int(_lib.load().qc_decode_work_words(self.plan.handle, gp)), dtype=i32, device=dev)
+        # early stop with lane compaction (es_compact.cu): a second lane set
+        nes = int(_lib.load().qc_decode_es_scratch_words(self.plan.handle, gp)) if (
+            self.early_stop and not self.fp64 and compact) else 0
+        self.es_scratch = torch.zeros(nes, dtype=i32, device=dev) if nes else None
         self.ok = torch.zeros(gp, dtype=torch.uint8, device=dev)
         self.iters = torch.zeros(gp, dtype=i32, device=dev)
         self.lane_bits = torch.zeros(gp, dtype=i32, device=dev) if count_bits else None
@@ -239,6 +243,12 @@ class BlockDecoder:
             if self.lane_bits is not None:
                 _lib.call("qc_bit_errors", self.plan.handle, self.gp, self.hb.data_ptr(),
                           self.lane_bits.data_ptr(), _stream())
+            return
+        if self.es_scratch is not None:
+            _lib.call("qc_decode_es", self.plan.handle, self.gp, self.iterations,
+                      self.mu.data_ptr(), self.msgs.data_ptr(), self.post.data_ptr(),
+                      self.hb.data_ptr(), self.work.data_ptr(), self.es_scratch.data_ptr(), self.ok.data_ptr(),
+                      self.iters.data_ptr(), _lib.ptr(self.lane_bits), _stream())
             return
         _lib.call("qc_decode", self.plan.handle, self.gp, self.iterations, int(self.early_stop),
                   self.mu.data_ptr(), self.msgs.data_ptr(), self.post.data_ptr(),
@@ -265,6 +275,8 @@ class BlockDecoder:
         if self.fp64:
             it = self.iterations
             n = (2 + 4 * it + 2) if self.early_stop else (1 + 2 * it + 2)
+        elif self.es_scratch is not None:
+            n = int(_lib.load().qc_decode_es_launches(self.plan.handle, self.gp, self.iterations))
         else:
             n = int(_lib.load().qc_decode_launches(self.plan.handle, self.gp, self.iterations,
                                                    int(self.early_stop)))

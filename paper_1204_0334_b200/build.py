@@ -23,7 +23,7 @@ OUT_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(OUT_DIR, "libqcldpc_b200.so")
 SOURCES = ["plan.cu", "block.cu", "vnu.cu", "cnu_dc4.cu", "cnu_dc8.cu", "cnu_dc16.cu", "cnu_dc24.cu",
            "cnu_dc32.cu", "recycle.cu", "block64.cu", "channel.cu", "stream.cu",
-           "host_pipe.cu", "agg.cu"]
+           "host_pipe.cu", "agg.cu", "es_compact.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden"]

@@ -52,7 +52,22 @@ struct AggArgs {
   int rows_eff;        // rows the grid covers (rows / items per thread, rounded up)
   const uint32_t* active;   // early stop: lane mask words (gamma / 32) or null
   const uint32_t* active2;  // early stop: second mask ANDed in (active = act & bad on the fly) or null
+  // compacted early-stop segments (es_compact.cu): *live lanes of the set are
+  // packed at the front of both halves (half A holds (live + 1) / 2, half B
+  // live / 2); the grid then walks only the lane groups holding them
+  const int32_t* live;
+  int live_half;            // 0: this window is half A, 1: half B
 };
+
+// lane groups of this window that hold live lanes (live mode)
+template <int VEC>
+__device__ __forceinline__ unsigned live_groups(const AggArgs& a) {
+  const int c = *a.live;
+  const int n = a.live_half ? (c >> 1) : ((c + 1) >> 1);
+  const int lpg = VEC << a.lg_gw;
+  return (unsigned)min(a.groups, (n + lpg - 1) / lpg);
+}
+
 
 // 32-lane word of the early-stop mask holding lane g0 (all on without one)
 __device__ __forceinline__ uint32_t es_word(const AggArgs& a, int g0) {
@@ -117,11 +132,14 @@ enum AggFlags { AGG_FIRST = AGG_FIRST_FLAG, AGG_LAST = AGG_LAST_FLAG, AGG_ES = 4
 // launch latency and index math of kernel k+1 overlap the tail of kernel k.
 // block (bx within its lane group, group index) + thread -> (row, lane vector q).
 // Lane-group major: every row of one group of lanes before the next group.
-__device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned grp, int& row, int& q) {
+// ngroups: groups the reversed order runs over (a.groups, or the live ones of a
+// compacted segment: then the groups written last are still visited first)
+__device__ __forceinline__ bool agg_map(const AggArgs& a, unsigned bx, unsigned grp, int& row, int& q,
+                                        int ngroups) {
   const unsigned idx = bx * AGG_THREADS + threadIdx.x;
   row = (int)(idx >> a.lg_gw);
   if (row >= a.rows_eff) return false;
-  const int g = a.reverse ? a.groups - 1 - (int)grp : (int)grp;
+  const int g = a.reverse ? ngroups - 1 - (int)grp : (int)grp;
   q = a.q0 + (g << a.lg_gw) + (int)(idx & ((1u << a.lg_gw) - 1u));
   return true;
 }
@@ -441,18 +459,58 @@ template <int DC, int VEC, bool FROM_MU>
 __global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
   int m, q;
-  const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q);
+  const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q, a.groups);
   pdl_wait();
   if (on) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
+}
+
+// Live mode (compacted early-stop segments, es_compact.cu): a capped grid whose
+// CTAs walk only the virtual blocks of the live lane groups.  Separate kernels,
+// so the loop's register needs never touch the fixed-iteration path (inlined
+// into it, the loop made the 64-register fused kernel spill 152 B).
+#ifndef AGG_LIVE_WAVES
+#define AGG_LIVE_WAVES 2
+#endif
+#ifndef AGG_LIVE_MINB
+#define AGG_LIVE_MINB AGG_VAR_MINB
+#endif
+constexpr unsigned LIVE_CTAS = 148 * 8 * AGG_LIVE_WAVES;
+
+template <int DC, int VEC>
+__global__ void __launch_bounds__(AGG_THREADS) agg_check_live_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
+  pdl_wait();
+  const unsigned bpg = (unsigned)((((long long)a.rows_eff << a.lg_gw) + AGG_THREADS - 1) / AGG_THREADS);
+  const unsigned lg = live_groups<VEC>(a), nv = lg * bpg;
+#pragma unroll 1
+  for (unsigned v = blockIdx.x; v < nv; v += gridDim.x) {
+    const unsigned g = v / bpg;
+    int m, q;
+    if (agg_map(a, v - g * bpg, g, m, q, lg)) check_body<DC, VEC, false>(a, grid, m, q);
+  }
 }
 
 template <int DV, int VEC, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
   int n, q;
-  const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q);
+  const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q, a.groups);
   pdl_wait();
   if (on) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
+}
+
+template <int DV, int VEC, int FLAGS, int ITEMS>
+__global__ void __launch_bounds__(AGG_THREADS, AGG_LIVE_MINB) agg_var_live_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
+  pdl_wait();
+  const unsigned bpg = (unsigned)((((long long)a.rows_eff << a.lg_gw) + AGG_THREADS - 1) / AGG_THREADS);
+  const unsigned lg = live_groups<VEC>(a), nv = lg * bpg;
+#pragma unroll 1
+  for (unsigned v = blockIdx.x; v < nv; v += gridDim.x) {
+    const unsigned g = v / bpg;
+    int n, q;
+    if (agg_map(a, v - g * bpg, g, n, q, lg)) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
+  }
 }
 
 // Early stop folded into the fused launches (bp.py:242-256).  Per-lane state,
@@ -543,27 +601,50 @@ __device__ __forceinline__ void es_update_block(const EsFused& e) {
   }
 }
 
+// one block (bx, by) of the fused grid; gv / gc: lane groups the variable /
+// check job visits (all, or the live ones of a compacted segment)
 template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
-__global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void fused_block(const FusedArgs& f, const QcGrid& grid, unsigned bx, unsigned by,
+                                            unsigned gv, unsigned gc) {
   int row, q;
-  if (blockIdx.y < f.es_rows) {              // early-stop bookkeeping blocks, scheduled first
-    const unsigned e = blockIdx.y * (f.R + 1) + blockIdx.x;
+  if (by < f.es_rows) {                      // early-stop bookkeeping blocks, scheduled first
+    const unsigned e = by * (f.R + 1) + bx;
     if (e < (unsigned)f.es.nbs) es_syndrome_block<DC>(f.es, grid, e, f.c.rows);
     else if (e == (unsigned)f.es.nbs && f.es.u_W > 0) es_update_block(f.es);
     return;
   }
-  const unsigned y = blockIdx.y - f.es_rows;
-  if (blockIdx.x == f.R) {
+  const unsigned y = by - f.es_rows;
+  if (bx == f.R) {
     const unsigned b = y, g = div_magic(b, f.c_magic);
-    if (agg_map(f.c, b - g * f.c_bpg, g, row, q)) check_body<DC, VC, FROM_MU>(f.c, grid, row, q);
+    if (g < gc && agg_map(f.c, b - g * f.c_bpg, g, row, q, min(gc, (unsigned)f.c.groups)))
+      check_body<DC, VC, FROM_MU>(f.c, grid, row, q);
   } else {
-    const unsigned b = y * f.R + blockIdx.x;
+    const unsigned b = y * f.R + bx;
     if (b >= f.nbv) return;
     const unsigned g = div_magic(b, f.v_magic);
-    if (agg_map(f.v, b - g * f.v_bpg, g, row, q)) var_items<DV, VV, FLAGS, ITEMS>(f.v, grid, row, q);
+    if (g < gv && agg_map(f.v, b - g * f.v_bpg, g, row, q, min(gv, (unsigned)f.v.groups)))
+      var_items<DV, VV, FLAGS, ITEMS>(f.v, grid, row, q);
   }
+}
+
+template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
+__global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
+  pdl_wait();
+  fused_block<DC, DV, VC, VV, FROM_MU, FLAGS, ITEMS>(f, grid, blockIdx.x, blockIdx.y, 0xffffffffu, 0xffffffffu);
+}
+
+// live mode: grid rows that hold live lane groups only, walked by a capped grid
+template <int DC, int DV, int VC, int VV, int FLAGS, int ITEMS>
+__global__ void __launch_bounds__(AGG_THREADS, AGG_LIVE_MINB) agg_fused_live_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
+  pdl_trigger();
+  pdl_wait();
+  const unsigned gv = live_groups<VV>(f.v), gc = live_groups<VC>(f.c);
+  const unsigned rows = f.es_rows + max(gc * f.c_bpg, (gv * f.v_bpg + f.R - 1) / f.R);
+  const unsigned nv = rows * (f.R + 1);
+#pragma unroll 1
+  for (unsigned v = blockIdx.y * gridDim.x + blockIdx.x; v < nv; v += gridDim.x * gridDim.y)
+    fused_block<DC, DV, VC, VV, false, FLAGS, ITEMS>(f, grid, v % (f.R + 1), v / (f.R + 1), gv, gc);
 }
 
 namespace {
@@ -620,7 +701,9 @@ unsigned blocks_per_group(const AggArgs& a) {
   return (unsigned)((((long long)a.rows_eff << a.lg_gw) + AGG_THREADS - 1) / AGG_THREADS);
 }
 
-dim3 agg_grid(const AggArgs& a, int) { return dim3(blocks_per_group(a), (unsigned)a.groups, 1); }
+dim3 agg_grid(const AggArgs& a, int) {
+  return dim3(blocks_per_group(a), (unsigned)a.groups, 1);
+}
 
 // pass arguments over the lane window [lane0, lane0 + lanes) of a gamma-wide store
 AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_t* hb, int rows, int gamma,
@@ -631,10 +714,15 @@ AggArgs make_args(float* msgs, const float* mu, float* agg, float* post, uint32_
   return a;
 }
 
+dim3 live_grid(const AggArgs& a) {
+  return dim3(std::min(blocks_per_group(a) * (unsigned)a.groups, LIVE_CTAS), 1, 1);
+}
+
 template <int DC, int VEC>
 void launch_check_v(const AggArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
-  if (from_mu) launch_k(agg_check_kernel<DC, VEC, true>, nb, s, a, g);
+  if (a.live) launch_k(agg_check_live_kernel<DC, VEC>, live_grid(a), s, a, g);   // never from mu
+  else if (from_mu) launch_k(agg_check_kernel<DC, VEC, true>, nb, s, a, g);
   else launch_k(agg_check_kernel<DC, VEC, false>, nb, s, a, g);
 }
 
@@ -648,32 +736,42 @@ void launch_check_dc(const AggArgs& a, int vec, bool from_mu, const QcGrid& g, c
 }
 
 template <int DV, int VEC, int ITEMS>
-void launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
+int launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
+  if (a.live) {        // compacted early-stop segment: its last variable pass
+    if (flags == AGG_ES) launch_k(agg_var_live_kernel<DV, VEC, AGG_ES, ITEMS>, live_grid(a), s, a, g);
+    else if (flags == (AGG_ES | AGG_LAST))
+      launch_k(agg_var_live_kernel<DV, VEC, AGG_ES | AGG_LAST, ITEMS>, live_grid(a), s, a, g);
+    else return fail_arg("live variable pass: unsupported flags");
+    return 0;
+  }
   switch (flags) {
     case 0: launch_k(agg_var_kernel<DV, VEC, 0, ITEMS>, nb, s, a, g); break;
     case AGG_FIRST: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST, ITEMS>, nb, s, a, g); break;
     case AGG_LAST: launch_k(agg_var_kernel<DV, VEC, AGG_LAST, ITEMS>, nb, s, a, g); break;
+    case AGG_FIRST | AGG_LAST: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS>, nb, s, a, g); break;
+    case AGG_ES: launch_k(agg_var_kernel<DV, VEC, AGG_ES, ITEMS>, nb, s, a, g); break;
     case AGG_ES | AGG_LAST: launch_k(agg_var_kernel<DV, VEC, AGG_ES | AGG_LAST, ITEMS>, nb, s, a, g); break;
     case AGG_ES | AGG_FIRST | AGG_LAST:
       launch_k(agg_var_kernel<DV, VEC, AGG_ES | AGG_FIRST | AGG_LAST, ITEMS>, nb, s, a, g);
       break;
-    default: launch_k(agg_var_kernel<DV, VEC, AGG_FIRST | AGG_LAST, ITEMS>, nb, s, a, g);
+    default: return fail_arg("compact variable pass: unsupported flags");
   }
+  return 0;
 }
 
 template <int DV, int VEC>
-void launch_var_v(AggArgs a, int flags, const QcGrid& g, cudaStream_t s) {
+int launch_var_v(AggArgs a, int flags, const QcGrid& g, cudaStream_t s) {
   a.rows_eff = (a.rows + AGG_ITEMS - 1) / AGG_ITEMS;      // standalone variable pass: AGG_ITEMS rows per thread
-  launch_var_i<DV, VEC, AGG_ITEMS>(a, flags, g, s);
+  return launch_var_i<DV, VEC, AGG_ITEMS>(a, flags, g, s);
 }
 
 template <int DV>
-void launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaStream_t s) {
+int launch_var_dv(const AggArgs& a, int vec, int flags, const QcGrid& g, cudaStream_t s) {
   switch (vec) {
-    case 4: launch_var_v<DV, 4>(a, flags, g, s); break;
-    case 2: launch_var_v<DV, 2>(a, flags, g, s); break;
-    default: launch_var_v<DV, 1>(a, flags, g, s);
+    case 4: return launch_var_v<DV, 4>(a, flags, g, s);
+    case 2: return launch_var_v<DV, 2>(a, flags, g, s);
+    default: return launch_var_v<DV, 1>(a, flags, g, s);
   }
 }
 
@@ -688,6 +786,15 @@ void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t
 
 template <int DC, int DV, int VC>
 int launch_fused_v(const FusedArgs& f, dim3 grid, bool from_mu, int flags, const QcGrid& g, cudaStream_t s) {
+  if (f.v.live) {      // compacted early-stop segment (never the first iteration)
+    const dim3 lg(f.R + 1, std::min(grid.y, (LIVE_CTAS + f.R) / (f.R + 1)), 1);
+    if (!from_mu && flags == AGG_ES)
+      launch_k(agg_fused_live_kernel<DC, DV, VC, AGG_FUSED_VV, AGG_ES, AGG_ITEMS>, lg, s, f, g);
+    else if (!from_mu && flags == (AGG_ES | AGG_LAST))
+      launch_k(agg_fused_live_kernel<DC, DV, VC, AGG_FUSED_VV, AGG_ES | AGG_LAST, AGG_ITEMS>, lg, s, f, g);
+    else return fail_arg("live fused pass: unsupported (from_mu, flags) combination");
+    return 0;
+  }
   if (from_mu && flags == AGG_FIRST) launch_fused_t<DC, DV, VC, true, AGG_FIRST>(f, grid, g, s);
   else if (from_mu && flags == (AGG_FIRST | AGG_LAST)) launch_fused_t<DC, DV, VC, true, AGG_FIRST | AGG_LAST>(f, grid, g, s);
   else if (!from_mu && flags == AGG_FIRST) launch_fused_t<DC, DV, VC, false, AGG_FIRST>(f, grid, g, s);
@@ -720,7 +827,7 @@ bool agg_fused_eligible(const qc_plan* p, int gamma) {
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
                         const uint32_t* v_act, const uint32_t* v_act2, const uint32_t* c_act, const EsFused* es,
-                        cudaStream_t s);
+                        cudaStream_t s, const int32_t* live = nullptr);
 
 // variable pass on lanes [v0, v0 + lanes) fused with the check pass on lanes [c0, c0 + lanes)
 int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
@@ -732,7 +839,7 @@ int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, 
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
                         const uint32_t* v_act, const uint32_t* v_act2, const uint32_t* c_act, const EsFused* es,
-                        cudaStream_t s) {
+                        cudaStream_t s, const int32_t* live) {
   FusedArgs f;
   f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, AGG_REVERSE);
   f.v.rows_eff = (f.v.rows + AGG_ITEMS - 1) / AGG_ITEMS;
@@ -740,6 +847,9 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
   f.v.active = v_act;
   f.v.active2 = v_act2;
   f.c.active = c_act;
+  f.v.live = f.c.live = live;
+  f.v.live_half = v0 >= gamma / 2;
+  f.c.live_half = c0 >= gamma / 2;
   f.v_bpg = blocks_per_group(f.v);
   f.c_bpg = blocks_per_group(f.c);
   f.v_magic = magic40(f.v_bpg);
@@ -766,10 +876,11 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
 
 // single passes over a lane window (active, active2: early-stop masks ANDed)
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active = nullptr);
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active = nullptr,
+                       const int32_t* live = nullptr);
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active = nullptr,
-                     const uint32_t* active2 = nullptr);
+                     const uint32_t* active2 = nullptr, const int32_t* live = nullptr);
 
 bool agg_eligible(const qc_plan* p) {
   return agg_mode() != 0 && p && p->qc_regular && p->E > 0 && dc_supported(p->L) && dv_supported(p->J) &&
@@ -786,10 +897,12 @@ int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, con
 }
 
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active) {
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active, const int32_t* live) {
   const int vec = pick_vec(lanes);
   AggArgs a = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, lane0, lanes, vec, 0);
   a.active = active;
+  a.live = live;
+  a.live_half = lane0 >= gamma / 2;
   const QcGrid g = make_grid(p);
   switch (p->L) {
     case 4: launch_check_dc<4>(a, vec, from_mu, g, s); break;
@@ -811,19 +924,23 @@ int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const fl
 
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active,
-                     const uint32_t* active2) {
+                     const uint32_t* active2, const int32_t* live) {
   const int vec = pick_vec_var(lanes);
   AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
                         AGG_REVERSE);
   a.active = active;
   a.active2 = active2;
+  a.live = live;
+  a.live_half = lane0 >= gamma / 2;
   const QcGrid g = make_grid(p);
+  int rc;
   switch (p->J) {
-    case 2: launch_var_dv<2>(a, vec, flags, g, s); break;
-    case 3: launch_var_dv<3>(a, vec, flags, g, s); break;
-    case 4: launch_var_dv<4>(a, vec, flags, g, s); break;
+    case 2: rc = launch_var_dv<2>(a, vec, flags, g, s); break;
+    case 3: rc = launch_var_dv<3>(a, vec, flags, g, s); break;
+    case 4: rc = launch_var_dv<4>(a, vec, flags, g, s); break;
     default: return fail_arg("compact schedule: unsupported variable degree");
   }
+  if (rc) return rc;
   return check_launch("agg_var");
 }
 
@@ -885,15 +1002,23 @@ int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2
                    uint32_t* bad_fin, uint8_t* ok, int32_t* iters_run, const float* post, uint32_t* hb,
                    cudaStream_t s);
 
-int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
-                      uint32_t* hb, uint32_t* es_words, uint8_t* ok, int32_t* iters_run, cudaStream_t s) {
+// Iterations [t0, t1] of the compact early-stop decode (t1 <= iters).  t0 == 1:
+// the decode's start (fused init, every lane active).  t0 > 1: a continuation
+// on a compacted lane set (es_compact.cu) whose active mask is already in
+// act[t0 & 1], with bad[(t0-1) & 1] = all ones and bad[t0 & 1] = bad_fin = 0,
+// so active_{t0-1} = act & bad is that mask; iters_run holds `iters` there.
+// The segment ends with the variable pass of half B at t1 (packages written
+// unless t1 == iters: the last beta is never read).
+int run_agg_es_segment(const qc_plan* p, int gamma, int t0, int t1, int iters, float* msgs, const float* mu,
+                       float* agg, float* post, uint32_t* hb, uint32_t* es_words, int32_t* iters_run,
+                       cudaStream_t s, const int32_t* live) {
   const int W = gamma / 32, H = gamma / 2, A = 0, B = H, WH = W / 2;
   uint32_t* act[2] = {es_words, es_words + W};
   uint32_t* bad[2] = {es_words + 2 * W, es_words + 3 * W};
-  uint32_t* bad_fin = es_words + 4 * W;
+  const bool fresh = t0 == 1;
   int rc;
-  cudaMemsetAsync(bad_fin, 0, sizeof(uint32_t) * W, s);
-  if ((rc = launch_agg_check_w(p, gamma, A, H, true, msgs, mu, agg, s))) return rc;
+  if ((rc = launch_agg_check_w(p, gamma, A, H, fresh, msgs, mu, agg, s, fresh ? nullptr : act[t0 & 1], live)))
+    return rc;
   auto es_for = [&](int t, int vw0, int sw0, bool syn) {
     EsFused e{};
     e.hb = hb;
@@ -916,25 +1041,39 @@ int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const
     e.u_iters = iters;
     return e;
   };
-  for (int t = 1; t <= iters; ++t) {
+  for (int t = t0; t <= t1; ++t) {
     const int vflags = AGG_ES | (t == 1 ? AGG_FIRST : 0) | (t == iters ? AGG_LAST : 0);
     const uint32_t* vm = t == 1 ? nullptr : act[t & 1];        // active_{t-1} = act[t&1] & bad[(t-1)&1]
     const uint32_t* vm2 = t == 1 ? nullptr : bad[(t - 1) & 1];
     // V(A, t) + C(B, t) + S(B, t-1) + U(A, t); C(B, t) masked by active_{t-2}(B) = act[t&1]
-    EsFused e1 = es_for(t, A / 32, B / 32, t > 1);
+    // (a continuation's first launch skips S(B, t0-1): bad[(t0-1)&1] is preset)
+    EsFused e1 = es_for(t, A / 32, B / 32, t > t0);
     if ((rc = launch_agg_fused_es(p, gamma, H, A, vflags, B, t == 1, msgs, mu, agg, post, hb, vm, vm2,
-                                  t <= 2 ? nullptr : act[t & 1], &e1, s)))
+                                  (fresh && t <= 2) ? nullptr : act[t & 1], &e1, s, live)))
       return rc;
     // V(B, t) + C(A, t+1) + S(A, t) + U(B, t); C(A, t+1) masked by active_{t-1}(A) = act[(t-1)&1]
     EsFused e2 = es_for(t, B / 32, A / 32, true);
-    if (t < iters) {
+    if (t < t1) {
       if ((rc = launch_agg_fused_es(p, gamma, H, B, vflags, A, false, msgs, mu, agg, post, hb, vm, vm2,
-                                    act[(t - 1) & 1], &e2, s)))
+                                    act[(t - 1) & 1], &e2, s, live)))
         return rc;
-    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, vm, vm2))) {
+    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, vm, vm2, live))) {
       return rc;
     }
   }
+  return 0;
+}
+
+int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
+                      uint32_t* hb, uint32_t* es_words, uint8_t* ok, int32_t* iters_run, cudaStream_t s) {
+  const int W = gamma / 32;
+  uint32_t* act[2] = {es_words, es_words + W};
+  uint32_t* bad[2] = {es_words + 2 * W, es_words + 3 * W};
+  uint32_t* bad_fin = es_words + 4 * W;
+  cudaMemsetAsync(bad_fin, 0, sizeof(uint32_t) * W, s);
+  if (int rc = run_agg_es_segment(p, gamma, 1, iters, iters, msgs, mu, agg, post, hb, es_words, iters_run, s,
+                                  nullptr))
+    return rc;
   return launch_es_tail(p, gamma, iters, act, bad, bad_fin, ok, iters_run, post, hb, s);
 }
 

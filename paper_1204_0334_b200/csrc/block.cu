@@ -310,6 +310,11 @@ int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2
 int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s) {
   return launch_syndrome(p, gamma, hb, bad, nullptr, s);
 }
+int launch_hard_bits_ext(const qc_plan* p, int gamma, const float* post, uint32_t* hb, cudaStream_t s) {
+  long long threads = (long long)p->N * (gamma / 4);
+  hard_bits_kernel<<<blocks_for(threads), THREADS, 0, s>>>(post, hb, p->N, gamma);
+  return check_launch("hard_bits");
+}
 int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s) {
   return launch_bit_errors(p, gamma, hb, lane_bits, s);
 }
@@ -451,6 +456,29 @@ int qc_decode(const qc_plan* p, int gamma, int iters, int early_stop, const floa
   }
   if (lane_bits && (rc = launch_bit_errors(p, gamma, hb, lane_bits, s))) return rc;
   return check_launch("decode");
+}
+
+int qc_decode_es(const qc_plan* p, int gamma, int iters, const float* mu, float* msgs, float* post, uint32_t* hb,
+                 uint32_t* work, uint32_t* scratch, uint8_t* ok, int32_t* iters_run, int32_t* lane_bits,
+                 void* stream) {
+  if (int r = check_gamma(gamma)) return r;
+  if (iters < 1) return fail_arg("need at least one iteration");
+  if (!p || !mu || !msgs || !post || !hb || !work || !ok || !iters_run) return fail_arg("null argument");
+  if (!es_compact_eligible(p, gamma, iters))
+    return qc_decode(p, gamma, iters, 1, mu, msgs, post, hb, work, ok, iters_run, lane_bits, stream);
+  if (!scratch) return fail_arg("null scratch (qc_decode_es_scratch_words > 0)");
+  cudaStream_t s = as_stream(stream);
+  int rc;
+  if ((rc = run_agg_decode_es_compact(p, gamma, iters, msgs, mu, post, hb, work, scratch, ok, iters_run, s)))
+    return rc;
+  if (lane_bits && (rc = launch_bit_errors(p, gamma, hb, lane_bits, s))) return rc;
+  return check_launch("decode_es");
+}
+
+int qc_decode_es_launches(const qc_plan* p, int gamma, int iters) {
+  if (!p || iters < 1) return -1;
+  if (!es_compact_eligible(p, gamma, iters)) return qc_decode_launches(p, gamma, iters, 1);
+  return es_compact_launches(p, gamma, iters);
 }
 
 int qc_lane_major(int n, int gamma, int gamma_out, const float* post, double* post_out, uint8_t* bits_out,

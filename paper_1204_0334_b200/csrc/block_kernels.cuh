@@ -299,6 +299,21 @@ int agg_decode_launches(const qc_plan* p, int gamma, int iters);
 bool agg_es_eligible(const qc_plan* p, int gamma);
 int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* agg, float* post,
                       uint32_t* hb, uint32_t* es_words, uint8_t* ok, int32_t* iters_run, cudaStream_t s);
+int run_agg_es_segment(const qc_plan* p, int gamma, int t0, int t1, int iters, float* msgs, const float* mu,
+                       float* agg, float* post, uint32_t* hb, uint32_t* es_words, int32_t* iters_run,
+                       cudaStream_t s, const int32_t* live);
+int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2], uint32_t* const bad[2],
+                   uint32_t* bad_fin, uint8_t* ok, int32_t* iters_run, const float* post, uint32_t* hb,
+                   cudaStream_t s);
+int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s);
+int launch_hard_bits_ext(const qc_plan* p, int gamma, const float* post, uint32_t* hb, cudaStream_t s);
+int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s);
+bool es_compact_eligible(const qc_plan* p, int gamma, int iters);
+size_t es_compact_words(const qc_plan* p, int gamma);
+int run_agg_decode_es_compact(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* post,
+                              uint32_t* hb, uint32_t* work, uint32_t* scratch, uint8_t* ok, int32_t* iters_run,
+                              cudaStream_t s);
+int es_compact_launches(const qc_plan* p, int gamma, int iters);
 size_t work_head_words(int gamma);
 bool agg_fused_eligible(const qc_plan* p, int gamma);
 int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,

@@ -556,3 +556,63 @@ def test_packages_view_semantics(gpu):
     q.check_node_update(b, lay)
     obp.check_update(ob, olay)
     close(b.packages, ob[:-1])
+
+
+@pytest.mark.parametrize("db,G,it", [("3.2", 1024, 30), ("3.0", 512, 30), ("3.6", 256, 30), ("3.3", 768, 14),
+                                     ("3.2", 256, 40), ("3.4", 512, 11), ("3.4", 512, 10)])
+def test_compacted_early_stop_matches_uncompacted(gpu, db, G, it):
+    """Early stop with lane compaction (qc_decode_es: continuing lanes packed
+    into a second buffer set at checkpoint iterations 10/13/17/22) equals the
+    uncompacted compact-schedule early-stop decode bit for bit -- posteriors at
+    each lane's freeze iteration, hard-bit planes, syndrome flags, iteration
+    counts, per-lane bit counts -- at waterfall, high-error and high-SNR points,
+    for 1-4 checkpoints and for iteration caps at / below the first one."""
+    import torch
+    from paper_1204_0334_b200 import _lib
+    q = gpu
+    h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
+    lay = q.build_edge_layout(h)
+    sigma = q.ebn0_to_sigma(float(db), 1 - lay.n_checks / lay.n_vars)
+    outs = []
+    for compact in (False, True):
+        dec = q.BlockDecoder(lay, G, it, early_stop=True, graph=False, compact=compact)
+        assert (dec.es_scratch is not None) == compact
+        _lib.call("qc_channel", 9, 1, 77 * G, 0, lay.n_vars, G, sigma, dec.mu.data_ptr(), None, None, 0)
+        dec.run()
+        dec.run()                                   # repeat: scratch state from a previous decode is harmless
+        torch.cuda.synchronize()
+        outs.append([x.cpu().numpy() for x in (dec.post, dec.hb, dec.ok, dec.iters, dec.lane_bits)])
+    for k, (a, b) in enumerate(zip(*outs)):
+        assert np.array_equal(a, b), ("post", "hb", "ok", "iters", "lane_bits")[k]
+    its = outs[0][3]
+    if it == 30 and db == "3.2":
+        assert its.min() < 13 and its.max() > 17               # lanes finish in several segments
+
+
+def test_compacted_early_stop_against_oracle(gpu):
+    """decode through the compacted early-stop engine vs the float64 oracle's
+    early-stop decode on the same fixed-seed LLRs (bits, ok, iterations exact;
+    posteriors of converged lanes within the north-star tolerance)."""
+    import torch
+    from oracle import bp as obp
+    from oracle import qc as oqc
+    q = gpu
+    h, exp = q.load_code(q.codes.bundled_code_path("n18360"))
+    lay = q.build_edge_layout(h)
+    G = 256
+    sigma = q.ebn0_to_sigma(3.2, 1 - lay.n_checks / lay.n_vars)
+    y = q.simulate_block(q.ChannelConfig(3.2, 1 - lay.n_checks / lay.n_vars, seed=4, gamma=G), lay.n_vars)
+    dec = q.BlockDecoder(lay, G, 30, early_stop=True, graph=False)
+    assert dec.es_scratch is not None
+    dec.load_lane_major(y, sigma)
+    dec.run()
+    r = dec.result(G)
+    sel = np.arange(0, G, 16)                              # 16 lanes through the float64 oracle
+    olay = oqc.qc_layout(exp.shifts, exp.p)
+    bits, post, ok, its = obp.decode_llr(olay, obp.channel_llrs(y[sel], sigma), 30, early_stop=True)
+    assert np.array_equal(r.hard_bits[sel], bits)
+    assert np.array_equal(r.syndrome_ok[sel], ok)
+    assert np.array_equal(r.iterations_run[sel], its)
+    err = np.abs(r.posteriors[sel] - post) / np.maximum(np.abs(post), 1.0)
+    assert err[ok].max() <= 1e-4
+    assert len(set(its.tolist())) > 2
