@@ -361,6 +361,7 @@ class BlockDecoder:
 
 
 HOST_CHUNK = 512        # largest pipelined chunk of the host-buffer API (plan C/4, C/2, C.., C/2, C/4; tools/e2e_bench.py)
+HOST_CHUNK_ES = 1024    # chunk of early-stop batches from 2048 lanes (lane compaction needs >= 1024)
 HOST_SLOTS = 4          # CUDA streams (device buffer sets) the chunks rotate over, pageable input
 HOST_SLOTS_PINNED = 3   # same for page-locked input (no host staging copy to hide; tools/e2e_bench.py)
 PINNED_MIN_BYTES = 1 << 20
@@ -454,6 +455,10 @@ def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: b
         chunk = (gamma + 63) // 64 * 64
     else:
         chunk = min(HOST_CHUNK, max(128, ((gamma + 1) // 2 + 63) // 64 * 64))
+    if early_stop and gamma >= 2 * HOST_CHUNK_ES:
+        # early stop: chunks large enough for lane compaction (es_compact.cu,
+        # from 1024 lanes) -- profiles/r02/es_compaction.md
+        chunk = HOST_CHUNK_ES
     slots = (HOST_SLOTS_PINNED if pinned_input else HOST_SLOTS) if gamma > chunk else 1
     cache = layout.__dict__.setdefault("_host_decoders", {})
     key = (chunk, slots, iterations, bool(early_stop), torch.cuda.current_device())

@@ -199,9 +199,15 @@ size_t al64(size_t w) { return (w + 63) / 64 * 64; }
 
 }  // namespace
 
+// from 1024 lanes up: each half then has >= 4 lane groups of 128, so packing
+// can shrink the work (at 256 / 512 lanes it measured slower than the plain
+// early-stop decode, profiles/r02/es_compaction.md)
+constexpr int ES_COMPACT_MIN_GAMMA = 1024;
+
 bool es_compact_eligible(const qc_plan* p, int gamma, int iters) {
   int ck[MAX_CHECKPOINTS];
-  return agg_es_eligible(p, gamma) && gamma <= 65536 && n_checkpoints(iters, ck) > 0;
+  return agg_es_eligible(p, gamma) && gamma >= ES_COMPACT_MIN_GAMMA && gamma <= 65536 &&
+         n_checkpoints(iters, ck) > 0;
 }
 
 // scratch words: two lane sets (mu, post: N x gamma; hb: N x gamma/32; ok;
@@ -326,7 +332,8 @@ int es_compact_launches(const qc_plan* p, int gamma, int iters) {
 extern "C" {
 
 size_t qc_decode_es_scratch_words(const qc_plan* p, int gamma) {
-  if (!p || gamma <= 0 || gamma % 32) return 0;
+  if (!p || gamma <= 0 || gamma % 32 || !qcb::agg_es_eligible(p, gamma) || gamma < qcb::ES_COMPACT_MIN_GAMMA)
+    return 0;
   return qcb::es_compact_words(p, gamma);
 }
 

@@ -56,6 +56,7 @@ struct Slot {
   float* post = nullptr;        // (N, chunk) fp32 posteriors
   uint32_t* hb = nullptr;       // (N, chunk/32) hard-bit planes
   uint32_t* work = nullptr;     // qc_decode scratch
+  uint32_t* es_scratch = nullptr;  // early stop with lane compaction (qc_decode_es), or null
   uint8_t* ok = nullptr;        // (chunk)
   int32_t* its = nullptr;       // (chunk)
   double* post_lm = nullptr;    // (chunk, N) fp64 lane-major posteriors
@@ -203,7 +204,7 @@ static void free_slot(Slot& s) {
   if (s.copied_in) cudaEventDestroy(s.copied_in);
   if (s.ready) cudaEventDestroy(s.ready);
   if (s.st) cudaStreamDestroy(s.st);
-  void* dev[] = {s.x, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, s.post_lm, s.bits_lm};
+  void* dev[] = {s.x, s.mu, s.msgs, s.post, s.hb, s.work, s.es_scratch, s.ok, s.its, s.post_lm, s.bits_lm};
   for (void* d : dev)
     if (d) cudaFree(d);
   void* host[] = {s.h_llr, s.h_post, s.h_bits, s.h_ok, s.h_its};
@@ -223,6 +224,13 @@ static int init_slot(qc_host_dec* h, Slot& s) {
   HP_CK(cudaMalloc(&s.post, N * C * sizeof(float)));
   HP_CK(cudaMalloc(&s.hb, N * (C / 32) * sizeof(uint32_t)));
   HP_CK(cudaMalloc(&s.work, qc_decode_work_words(p, h->chunk) * sizeof(uint32_t)));
+  if (h->early_stop) {
+    const size_t nes = qc_decode_es_scratch_words(p, h->chunk);
+    if (nes) {
+      HP_CK(cudaMalloc(&s.es_scratch, nes * sizeof(uint32_t)));
+      HP_CK(cudaMemsetAsync(s.es_scratch, 0, nes * sizeof(uint32_t), s.st));
+    }
+  }
   HP_CK(cudaMalloc(&s.ok, C));
   HP_CK(cudaMalloc(&s.its, C * sizeof(int32_t)));
   HP_CK(cudaMalloc(&s.post_lm, C * N * sizeof(double)));
@@ -241,8 +249,13 @@ static int init_slot(qc_host_dec* h, Slot& s) {
     s.size[i] = c;
     cudaGraph_t g = nullptr;
     HP_CK(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
-    int rc = qc_decode(p, c, h->iters, h->early_stop, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its, nullptr,
-                       s.st);
+    // early stop: lane compaction where the plan / size allow it (else qc_decode_es
+    // falls back to qc_decode's early-stop path)
+    int rc = (h->early_stop && s.es_scratch)
+                 ? qc_decode_es(p, c, h->iters, s.mu, s.msgs, s.post, s.hb, s.work, s.es_scratch, s.ok, s.its,
+                                nullptr, s.st)
+                 : qc_decode(p, c, h->iters, h->early_stop, s.mu, s.msgs, s.post, s.hb, s.work, s.ok, s.its,
+                             nullptr, s.st);
     cudaError_t ce = cudaStreamEndCapture(s.st, &g);
     if (rc) {
       if (g) cudaGraphDestroy(g);

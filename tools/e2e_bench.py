@@ -19,6 +19,9 @@ def main():
     ap.add_argument("--chunks", default="256,512,1024")
     ap.add_argument("--slots", default="2,3,4")
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--early-stop", action="store_true")
+    ap.add_argument("--ebn0", type=float, default=3.2)
+    ap.add_argument("--pinned-only", action="store_true")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -27,22 +30,22 @@ def main():
     h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
     lay = q.build_edge_layout(h)
     N, K = lay.n_vars, lay.n_vars - lay.n_checks
-    sigma = q.ebn0_to_sigma(3.2, K / N)
+    sigma = q.ebn0_to_sigma(args.ebn0, K / N)
     y_pg = 1.0 + sigma * np.random.default_rng(0).standard_normal((args.gamma, N))
     y_pin = q.host_array(y_pg)
     for c in map(int, args.chunks.split(",")):
         for s in map(int, args.slots.split(",")):
-            qbp.HOST_CHUNK, qbp.HOST_SLOTS = c, s
+            qbp.HOST_CHUNK, qbp.HOST_SLOTS, qbp.HOST_SLOTS_PINNED = c, s, s
             lay.__dict__.pop("_host_decoders", None)
             torch.cuda.empty_cache()
-            rec = {"chunk": c, "slots": s}
-            for name, y in (("pinned", y_pin), ("pageable", y_pg)):
+            rec = {"chunk": c, "slots": s, "early_stop": args.early_stop, "ebn0_db": args.ebn0, "gamma": args.gamma}
+            for name, y in ((("pinned", y_pin),) if args.pinned_only else (("pinned", y_pin), ("pageable", y_pg))):
                 for _ in range(2):
-                    r = q.decode_batch(lay, y, sigma, 30)
+                    r = q.decode_batch(lay, y, sigma, 30, early_stop=args.early_stop)
                 del r
                 t0 = time.perf_counter()
                 for _ in range(args.steps):
-                    r = q.decode_batch(lay, y, sigma, 30)
+                    r = q.decode_batch(lay, y, sigma, 30, early_stop=args.early_stop)
                     del r
                 dt = (time.perf_counter() - t0) / args.steps
                 rec[name + "_mbit_s"] = round(args.gamma * K / dt / 1e6, 1)
