@@ -44,28 +44,30 @@ __global__ void __launch_bounds__(THREADS) channel_kernel(ChanArgs a) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // 32-bit index math (the host keeps blocks x gamma < 2^31): a 64-bit
+  // division / remainder per thread was ~8% of the kernel's instructions
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (a.t_dev) a.start += (uint64_t)((*a.t_dev + a.t_add) * a.t_mul);
   if (a.lane0_dev) a.lane0 = *a.lane0_dev;
   const uint64_t first = a.start >> 2;
-  const long long nblk = (long long)(((a.start & 3) + a.n + 3) >> 2);
-  if ((tid & ~31ll) >= nblk * a.gamma) return;    // whole warp out of range
-  const bool valid = tid < nblk * a.gamma;
-  int g = 0;
-  long long b = 0;
+  const unsigned off = (unsigned)(a.start & 3);
+  const unsigned total = ((off + (unsigned)a.n + 3u) >> 2) * (unsigned)a.gamma;
+  if ((tid & ~31u) >= total) return;    // whole warp out of range
+  const bool valid = tid < total;
+  unsigned g = 0, b = 0;
   if (valid) {
-    g = (int)(tid % a.gamma);
-    b = tid / a.gamma;
+    b = tid / (unsigned)a.gamma;
+    g = tid - b * (unsigned)a.gamma;
   }
   uint64_t w[4] = {0, 0, 0, 0};
   if (valid) philox4x64_10(first + (uint64_t)b + 1ull, a.lane0 + (uint64_t)g, 0ull, 0ull, a.k0, a.k1, w);
   const unsigned lt = (1u << lane) - 1u;
   int nc = 0, nt = 0;
   bool ok[4];
-  long long pos[4];
+  int pos[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    pos[k] = (long long)((first + (uint64_t)b) * 4ull + (uint64_t)k) - (long long)a.start;
+    pos[k] = (int)(b * 4u + (unsigned)k) - (int)off;      // (first + b) * 4 + k - start
     ok[k] = valid && pos[k] >= 0 && pos[k] < a.n;
     const double u = word_to_uniform(w[k]);
     const bool cen = ok[k] && ndtri_is_central(u);
@@ -113,6 +115,7 @@ int launch_channel(uint64_t k0, uint64_t k1, uint64_t lane0, uint64_t start, int
   long long nblk = (long long)(((start & 3) + (uint64_t)n + 3) >> 2);
   long long threads = nblk * gamma;
   if (threads == 0) return 0;
+  if (threads >= (1ll << 31)) return fail_arg("channel: n x gamma too large for one launch");
   launch_pdl(channel_kernel, dim3(blocks_for(threads)), THREADS, s, a);
   return check_launch("channel");
 }
@@ -130,6 +133,7 @@ int launch_channel_t(uint64_t k0, uint64_t k1, uint64_t lane0, const uint64_t* l
   // the start may be known only on the device: cover the worst-case block count
   long long threads = (long long)((n + 3) / 4 + 1) * gamma;
   if (threads == 0) return 0;
+  if (threads >= (1ll << 31)) return fail_arg("channel: n x gamma too large for one launch");
   launch_pdl(channel_kernel, dim3(blocks_for(threads)), THREADS, s, a);
   return check_launch("channel");
 }
