@@ -74,9 +74,14 @@ __global__ void hard_bits_kernel(const float* post, uint32_t* hb, int N, int gam
 // consecutive 32-lane words (coalesced), counts set bits in shared memory
 // (hard bits are sparse at useful SNRs: a zero word costs one load), and adds
 // its nonzero lane counts to the global ones
-__global__ void bit_errors_kernel(const uint32_t* hb, int32_t* lane_bits, int N, int W, int rows_per_block) {
-  extern __shared__ int cnt[];                 // W * 32 counters
+// lane_mask (W words, may be null): count only these lanes (the recycling
+// engine counts the lanes that finish this tick; the others' bits are discarded)
+__global__ void bit_errors_kernel(const uint32_t* hb, int32_t* lane_bits, int N, int W, int rows_per_block,
+                                  const uint32_t* lane_mask) {
+  extern __shared__ int cnt[];                 // W * 32 counters, then W mask words
+  uint32_t* msk = reinterpret_cast<uint32_t*>(cnt + W * 32);
   for (int i = threadIdx.x; i < W * 32; i += blockDim.x) cnt[i] = 0;
+  for (int i = threadIdx.x; i < W; i += blockDim.x) msk[i] = lane_mask ? lane_mask[i] : 0xffffffffu;
   __syncthreads();
   const int n0 = blockIdx.x * rows_per_block, n1 = min(N, n0 + rows_per_block);
   const long long total = (long long)(n1 - n0) * W;
@@ -87,12 +92,12 @@ __global__ void bit_errors_kernel(const uint32_t* hb, int32_t* lane_bits, int N,
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long i = i0 + (long long)u * blockDim.x;
-      x[u] = i < total ? base[i] : 0u;
+      x[u] = (i < total && msk[(int)(i % W)]) ? base[i] : 0u;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int w = (int)((i0 + (long long)u * blockDim.x) % W);
-      for (uint32_t v = x[u]; v; v &= v - 1) atomicAdd(&cnt[w * 32 + __ffs(v) - 1], 1);
+      for (uint32_t v = x[u] & msk[w]; v; v &= v - 1) atomicAdd(&cnt[w * 32 + __ffs(v) - 1], 1);
     }
   }
   __syncthreads();
@@ -246,20 +251,21 @@ int launch_syndrome(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* b
   return check_launch("syndrome");
 }
 
-int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s) {
+int launch_bit_errors(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s,
+                      const uint32_t* lane_mask = nullptr) {
   const int W = gamma / 32;
   cudaMemsetAsync(lane_bits, 0, sizeof(int32_t) * gamma, s);
   if (p->N == 0) return 0;
   // ~2 blocks per SM, each at least 64 rows; W * 32 counters of shared memory
   const int blocks = std::max(1, std::min(296, (p->N + 63) / 64));
   const int rows = (p->N + blocks - 1) / blocks;
-  const size_t smem = (size_t)W * 32 * sizeof(int);
+  const size_t smem = (size_t)W * 33 * sizeof(int);
   static const bool big_smem = [] {     // once per process (not a stream operation: graph-capture safe)
     return cudaFuncSetAttribute(bit_errors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ==
            cudaSuccess;
   }();
   if (smem > (big_smem ? 200u : 48u) * 1024) return fail_arg("bit_errors: gamma too large for the shared counters");
-  bit_errors_kernel<<<(p->N + rows - 1) / rows, 256, smem, s>>>(hb, lane_bits, p->N, W, rows);
+  bit_errors_kernel<<<(p->N + rows - 1) / rows, 256, smem, s>>>(hb, lane_bits, p->N, W, rows, lane_mask);
   return check_launch("bit_errors");
 }
 
@@ -315,8 +321,9 @@ int launch_hard_bits_ext(const qc_plan* p, int gamma, const float* post, uint32_
   hard_bits_kernel<<<blocks_for(threads), THREADS, 0, s>>>(post, hb, p->N, gamma);
   return check_launch("hard_bits");
 }
-int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s) {
-  return launch_bit_errors(p, gamma, hb, lane_bits, s);
+int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s,
+                          const uint32_t* lane_mask) {
+  return launch_bit_errors(p, gamma, hb, lane_bits, s, lane_mask);
 }
 }  // namespace qcb
 

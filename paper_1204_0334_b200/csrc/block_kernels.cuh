@@ -307,7 +307,8 @@ int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2
                    cudaStream_t s);
 int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s);
 int launch_hard_bits_ext(const qc_plan* p, int gamma, const float* post, uint32_t* hb, cudaStream_t s);
-int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s);
+int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s,
+                          const uint32_t* lane_mask = nullptr);
 bool es_compact_eligible(const qc_plan* p, int gamma, int iters);
 size_t es_compact_words(const qc_plan* p, int gamma);
 int run_agg_decode_es_compact(const qc_plan* p, int gamma, int iters, float* msgs, const float* mu, float* post,

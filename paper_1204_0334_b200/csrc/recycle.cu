@@ -28,7 +28,7 @@ namespace qcb {
 int launch_vnu(const qc_plan* p, VnuArgs a, int mode, cudaStream_t s);
 int launch_cnu_public(const qc_plan* p, CnuArgs a, int mode, cudaStream_t s);
 int launch_syndrome_ext(const qc_plan* p, int gamma, const uint32_t* hb, uint32_t* bad, cudaStream_t s);
-int launch_bit_errors_ext(const qc_plan* p, int gamma, const uint32_t* hb, int32_t* lane_bits, cudaStream_t s);
+
 
 namespace {
 
@@ -42,6 +42,7 @@ struct RcState {
   int32_t* fresh_count;    // [1]
   uint32_t* active;        // (W) lanes still iterating
   uint32_t* bad;           // (W) syndrome failures of this tick
+  uint32_t* fin;           // (W) lanes finishing this tick (frozen or capped)
   int64_t* next_group;     // [1] next group of codeword ids to hand out
   int64_t* counts;         // (n_batches, 3) frames, bit errors, frame errors
 };
@@ -169,6 +170,18 @@ __global__ void rc_finish_kernel(RcState s, RcConfig c) {
 
 __global__ void rc_reset_fresh_kernel(int32_t* fresh_count) { *fresh_count = 0; }
 
+// lanes that finish this tick (syndrome clean or at the iteration cap): the
+// only ones whose bit errors are counted (rc_finish_kernel)
+__global__ void rc_fin_mask_kernel(RcState s, RcConfig c) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = g < c.gamma;
+  bool f = false;
+  if (valid && ((s.active[g >> 5] >> (g & 31)) & 1u))
+    f = !((s.bad[g >> 5] >> (g & 31)) & 1u) || s.slot_it[g] + 1 >= c.max_it;
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if (valid && (g & 31) == 0) s.fin[g >> 5] = m;
+}
+
 }  // namespace
 }  // namespace qcb
 
@@ -186,7 +199,8 @@ RcState rc_state(void* base, int gamma) {
   s.fresh_list = reinterpret_cast<int32_t*>(p); p += (size_t)(gamma / GROUP) * 4;
   s.fresh_count = reinterpret_cast<int32_t*>(p); p += 8;
   s.active = reinterpret_cast<uint32_t*>(p); p += W * 4;
-  s.bad = reinterpret_cast<uint32_t*>(p);
+  s.bad = reinterpret_cast<uint32_t*>(p); p += W * 4;
+  s.fin = reinterpret_cast<uint32_t*>(p);
   s.counts = nullptr;
   return s;
 }
@@ -196,7 +210,7 @@ extern "C" {
 
 size_t qc_rc_state_bytes(int gamma) {
   const size_t G = (size_t)(gamma > 0 ? gamma : 0);
-  return G * 8 + 8 + G * 4 + G * 4 + (G / GROUP) * 4 + 8 + 2 * (G / 32) * 4 + 64;
+  return G * 8 + 8 + G * 4 + G * 4 + (G / GROUP) * 4 + 8 + 3 * (G / 32) * 4 + 64;
 }
 
 int qc_rc_init(int gamma, int64_t id_limit, void* state, void* stream) {
@@ -239,7 +253,8 @@ int qc_rc_ticks(const qc_plan* p, int gamma, int gamma_ref, int world, int rank,
     v.msgs = msgs; v.mu = mu; v.hb = hb; v.active = s.active; v.gamma = gamma;
     if ((rc = launch_vnu(p, v, VNU_PHI, st))) return rc;
     if ((rc = launch_syndrome_ext(p, gamma, hb, s.bad, st))) return rc;
-    if ((rc = launch_bit_errors_ext(p, gamma, hb, s.lane_bits, st))) return rc;
+    rc_fin_mask_kernel<<<blocks_for(gamma), THREADS, 0, st>>>(s, c);
+    if ((rc = launch_bit_errors_ext(p, gamma, hb, s.lane_bits, st, s.fin))) return rc;
     rc_finish_kernel<<<blocks_for(gamma), THREADS, 0, st>>>(s, c);
   }
   return check_launch("qc_rc_ticks");
