@@ -57,6 +57,8 @@ struct AggArgs {
   // live / 2); the grid then walks only the lane groups holding them
   const int32_t* live;
   int live_half;            // 0: this window is half A, 1: half B
+  int live_loop;            // 1: capped grid walking the live blocks (few live lanes);
+                            // 0: full grid, CTAs past the live rows exit at once
 };
 
 // lane groups of this window that hold live lanes (live mode)
@@ -459,7 +461,12 @@ template <int DC, int VEC, bool FROM_MU>
 __global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
   int m, q;
-  const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q, a.groups);
+  unsigned ng = a.groups;
+  if (a.live) {             // compacted segment, full grid: the lane count was written before it started
+    ng = live_groups<VEC>(a);
+    if (blockIdx.y >= ng) return;
+  }
+  const bool on = agg_map(a, blockIdx.x, blockIdx.y, m, q, ng);
   pdl_wait();
   if (on) check_body<DC, VEC, FROM_MU>(a, grid, m, q);
 }
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(AGG_THREADS) agg_check_kernel(AggArgs a, const
 #define AGG_LIVE_WAVES 2
 #endif
 #ifndef AGG_LIVE_MINB
-#define AGG_LIVE_MINB AGG_VAR_MINB
+#define AGG_LIVE_MINB 6   // 80 registers: the loop kernels do not spill (1-3% over 64 registers with spills)
 #endif
 constexpr unsigned LIVE_CTAS = 148 * 8 * AGG_LIVE_WAVES;
 
@@ -494,7 +501,12 @@ template <int DV, int VEC, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
   int n, q;
-  const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q, a.groups);
+  unsigned ng = a.groups;
+  if (a.live) {
+    ng = live_groups<VEC>(a);
+    if (blockIdx.y >= ng) return;
+  }
+  const bool on = agg_map(a, blockIdx.x, blockIdx.y, n, q, ng);
   pdl_wait();
   if (on) var_items<DV, VEC, FLAGS, ITEMS>(a, grid, n, q);
 }
@@ -630,6 +642,14 @@ __device__ __forceinline__ void fused_block(const FusedArgs& f, const QcGrid& gr
 template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
 __global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
+  if (f.v.live) {           // compacted segment, full grid: rows past the live lane groups exit at once
+    const unsigned gv = live_groups<VV>(f.v), gc = live_groups<VC>(f.c);
+    const unsigned rows = f.es_rows + max(gc * f.c_bpg, (gv * f.v_bpg + f.R - 1) / f.R);
+    if (blockIdx.y >= rows) return;
+    pdl_wait();
+    fused_block<DC, DV, VC, VV, FROM_MU, FLAGS, ITEMS>(f, grid, blockIdx.x, blockIdx.y, gv, gc);
+    return;
+  }
   pdl_wait();
   fused_block<DC, DV, VC, VV, FROM_MU, FLAGS, ITEMS>(f, grid, blockIdx.x, blockIdx.y, 0xffffffffu, 0xffffffffu);
 }
@@ -721,7 +741,7 @@ dim3 live_grid(const AggArgs& a) {
 template <int DC, int VEC>
 void launch_check_v(const AggArgs& a, bool from_mu, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
-  if (a.live) launch_k(agg_check_live_kernel<DC, VEC>, live_grid(a), s, a, g);   // never from mu
+  if (a.live && a.live_loop) launch_k(agg_check_live_kernel<DC, VEC>, live_grid(a), s, a, g);   // never from mu
   else if (from_mu) launch_k(agg_check_kernel<DC, VEC, true>, nb, s, a, g);
   else launch_k(agg_check_kernel<DC, VEC, false>, nb, s, a, g);
 }
@@ -738,7 +758,7 @@ void launch_check_dc(const AggArgs& a, int vec, bool from_mu, const QcGrid& g, c
 template <int DV, int VEC, int ITEMS>
 int launch_var_i(const AggArgs& a, int flags, const QcGrid& g, cudaStream_t s) {
   dim3 nb = agg_grid(a, VEC);
-  if (a.live) {        // compacted early-stop segment: its last variable pass
+  if (a.live && a.live_loop) {        // compacted early-stop segment: its last variable pass
     if (flags == AGG_ES) launch_k(agg_var_live_kernel<DV, VEC, AGG_ES, ITEMS>, live_grid(a), s, a, g);
     else if (flags == (AGG_ES | AGG_LAST))
       launch_k(agg_var_live_kernel<DV, VEC, AGG_ES | AGG_LAST, ITEMS>, live_grid(a), s, a, g);
@@ -786,7 +806,7 @@ void launch_fused_t(const FusedArgs& f, dim3 grid, const QcGrid& g, cudaStream_t
 
 template <int DC, int DV, int VC>
 int launch_fused_v(const FusedArgs& f, dim3 grid, bool from_mu, int flags, const QcGrid& g, cudaStream_t s) {
-  if (f.v.live) {      // compacted early-stop segment (never the first iteration)
+  if (f.v.live && f.v.live_loop) {      // compacted early-stop segment (never the first iteration)
     const dim3 lg(f.R + 1, std::min(grid.y, (LIVE_CTAS + f.R) / (f.R + 1)), 1);
     if (!from_mu && flags == AGG_ES)
       launch_k(agg_fused_live_kernel<DC, DV, VC, AGG_FUSED_VV, AGG_ES, AGG_ITEMS>, lg, s, f, g);
@@ -827,7 +847,7 @@ bool agg_fused_eligible(const qc_plan* p, int gamma) {
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
                         const uint32_t* v_act, const uint32_t* v_act2, const uint32_t* c_act, const EsFused* es,
-                        cudaStream_t s, const int32_t* live = nullptr);
+                        cudaStream_t s, const int32_t* live = nullptr, int live_loop = 0);
 
 // variable pass on lanes [v0, v0 + lanes) fused with the check pass on lanes [c0, c0 + lanes)
 int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu, float* msgs,
@@ -839,7 +859,7 @@ int launch_agg_fused(const qc_plan* p, int gamma, int lanes, int v0, int flags, 
 int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flags, int c0, bool from_mu,
                         float* msgs, const float* mu, float* agg, float* post, uint32_t* hb,
                         const uint32_t* v_act, const uint32_t* v_act2, const uint32_t* c_act, const EsFused* es,
-                        cudaStream_t s, const int32_t* live) {
+                        cudaStream_t s, const int32_t* live, int live_loop) {
   FusedArgs f;
   f.v = make_args(msgs, mu, agg, post, hb, p->N, gamma, v0, lanes, AGG_FUSED_VV, AGG_REVERSE);
   f.v.rows_eff = (f.v.rows + AGG_ITEMS - 1) / AGG_ITEMS;
@@ -848,6 +868,7 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
   f.v.active2 = v_act2;
   f.c.active = c_act;
   f.v.live = f.c.live = live;
+  f.v.live_loop = f.c.live_loop = live_loop;
   f.v.live_half = v0 >= gamma / 2;
   f.c.live_half = c0 >= gamma / 2;
   f.v_bpg = blocks_per_group(f.v);
@@ -877,10 +898,10 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
 // single passes over a lane window (active, active2: early-stop masks ANDed)
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
                        const float* mu, float* agg, cudaStream_t s, const uint32_t* active = nullptr,
-                       const int32_t* live = nullptr);
+                       const int32_t* live = nullptr, int live_loop = 0);
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active = nullptr,
-                     const uint32_t* active2 = nullptr, const int32_t* live = nullptr);
+                     const uint32_t* active2 = nullptr, const int32_t* live = nullptr, int live_loop = 0);
 
 bool agg_eligible(const qc_plan* p) {
   return agg_mode() != 0 && p && p->qc_regular && p->E > 0 && dc_supported(p->L) && dv_supported(p->J) &&
@@ -897,11 +918,13 @@ int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, con
 }
 
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
-                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active, const int32_t* live) {
+                       const float* mu, float* agg, cudaStream_t s, const uint32_t* active, const int32_t* live,
+                       int live_loop) {
   const int vec = pick_vec(lanes);
   AggArgs a = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, lane0, lanes, vec, 0);
   a.active = active;
   a.live = live;
+  a.live_loop = live_loop;
   a.live_half = lane0 >= gamma / 2;
   const QcGrid g = make_grid(p);
   switch (p->L) {
@@ -924,13 +947,14 @@ int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const fl
 
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active,
-                     const uint32_t* active2, const int32_t* live) {
+                     const uint32_t* active2, const int32_t* live, int live_loop) {
   const int vec = pick_vec_var(lanes);
   AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
                         AGG_REVERSE);
   a.active = active;
   a.active2 = active2;
   a.live = live;
+  a.live_loop = live_loop;
   a.live_half = lane0 >= gamma / 2;
   const QcGrid g = make_grid(p);
   int rc;
@@ -1011,13 +1035,14 @@ int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2
 // unless t1 == iters: the last beta is never read).
 int run_agg_es_segment(const qc_plan* p, int gamma, int t0, int t1, int iters, float* msgs, const float* mu,
                        float* agg, float* post, uint32_t* hb, uint32_t* es_words, int32_t* iters_run,
-                       cudaStream_t s, const int32_t* live) {
+                       cudaStream_t s, const int32_t* live, int live_loop) {
   const int W = gamma / 32, H = gamma / 2, A = 0, B = H, WH = W / 2;
   uint32_t* act[2] = {es_words, es_words + W};
   uint32_t* bad[2] = {es_words + 2 * W, es_words + 3 * W};
   const bool fresh = t0 == 1;
   int rc;
-  if ((rc = launch_agg_check_w(p, gamma, A, H, fresh, msgs, mu, agg, s, fresh ? nullptr : act[t0 & 1], live)))
+  if ((rc = launch_agg_check_w(p, gamma, A, H, fresh, msgs, mu, agg, s, fresh ? nullptr : act[t0 & 1], live,
+                               live_loop)))
     return rc;
   auto es_for = [&](int t, int vw0, int sw0, bool syn) {
     EsFused e{};
@@ -1049,15 +1074,16 @@ int run_agg_es_segment(const qc_plan* p, int gamma, int t0, int t1, int iters, f
     // (a continuation's first launch skips S(B, t0-1): bad[(t0-1)&1] is preset)
     EsFused e1 = es_for(t, A / 32, B / 32, t > t0);
     if ((rc = launch_agg_fused_es(p, gamma, H, A, vflags, B, t == 1, msgs, mu, agg, post, hb, vm, vm2,
-                                  (fresh && t <= 2) ? nullptr : act[t & 1], &e1, s, live)))
+                                  (fresh && t <= 2) ? nullptr : act[t & 1], &e1, s, live, live_loop)))
       return rc;
     // V(B, t) + C(A, t+1) + S(A, t) + U(B, t); C(A, t+1) masked by active_{t-1}(A) = act[(t-1)&1]
     EsFused e2 = es_for(t, B / 32, A / 32, true);
     if (t < t1) {
       if ((rc = launch_agg_fused_es(p, gamma, H, B, vflags, A, false, msgs, mu, agg, post, hb, vm, vm2,
-                                    act[(t - 1) & 1], &e2, s, live)))
+                                    act[(t - 1) & 1], &e2, s, live, live_loop)))
         return rc;
-    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, vm, vm2, live))) {
+    } else if ((rc = launch_agg_var_w(p, gamma, B, H, vflags, msgs, mu, agg, post, hb, s, vm, vm2, live,
+                                      live_loop))) {
       return rc;
     }
   }
@@ -1072,7 +1098,7 @@ int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const
   uint32_t* bad_fin = es_words + 4 * W;
   cudaMemsetAsync(bad_fin, 0, sizeof(uint32_t) * W, s);
   if (int rc = run_agg_es_segment(p, gamma, 1, iters, iters, msgs, mu, agg, post, hb, es_words, iters_run, s,
-                                  nullptr))
+                                  nullptr, 0))
     return rc;
   return launch_es_tail(p, gamma, iters, act, bad, bad_fin, ok, iters_run, post, hb, s);
 }

@@ -301,7 +301,7 @@ int run_agg_decode_es(const qc_plan* p, int gamma, int iters, float* msgs, const
                       uint32_t* hb, uint32_t* es_words, uint8_t* ok, int32_t* iters_run, cudaStream_t s);
 int run_agg_es_segment(const qc_plan* p, int gamma, int t0, int t1, int iters, float* msgs, const float* mu,
                        float* agg, float* post, uint32_t* hb, uint32_t* es_words, int32_t* iters_run,
-                       cudaStream_t s, const int32_t* live);
+                       cudaStream_t s, const int32_t* live, int live_loop);
 int launch_es_tail(const qc_plan* p, int gamma, int iters, uint32_t* const act[2], uint32_t* const bad[2],
                    uint32_t* bad_fin, uint8_t* ok, int32_t* iters_run, const float* post, uint32_t* hb,
                    cudaStream_t s);
