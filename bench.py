@@ -293,6 +293,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=120.0, help="reference arm time box (s)")
     ap.add_argument("--sustain-s", type=float, default=2.5, help="length of the sustained-rate window (0 = skip)")
     ap.add_argument("--no-curve", action="store_true", help="skip the decode_batch e2e gamma curve")
+    ap.add_argument("--no-es", action="store_true", help="skip the early-stop decode extra")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -511,6 +512,36 @@ def main():
 
     stream = stream_bench(args, q, rank, W, group, barrier) if args.stream_gamma else None
 
+    # ---- early stop (decode_llr_batch(..., early_stop=True) semantics, lane
+    # compaction from 1024 lanes): same code, channel and counters, gamma 4096,
+    # against the fixed 30-iteration decode at the same gamma ----
+    es = None
+    if not args.no_es:
+        GE, steps_es = 4096, 6
+        rates = {}
+        for name, flag in (("fixed", False), ("early_stop", True)):
+            e = q.BlockCampaign(lay, 32, GE // 32, ITERS, flag, seed=0)
+            for s in range(3):
+                e.step((s * W + rank) * GE, sigma)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for s in range(steps_es):
+                e.step(((3 + s) * W + rank) * GE, sigma)
+            b.record()
+            barrier()
+            t_ms = max_scalar(a.elapsed_time(b), group, device="cuda") / steps_es
+            rates[name] = (round(GE * W * K_info / (t_ms / 1e3) / 1e6, 2), round(t_ms, 3),
+                           float(e.dec.iters[:GE].float().mean().item()), e.kernel_launches_per_step())
+            del e
+            torch.cuda.empty_cache()
+        es = {"value": rates["early_stop"][0], "unit": "Mbit/s", "gamma": GE, "ebn0_db": EBN0,
+              "ms_per_step": rates["early_stop"][1], "mean_iterations": round(rates["early_stop"][2], 2),
+              "fixed_value": rates["fixed"][0], "fixed_ms_per_step": rates["fixed"][1],
+              "speedup_vs_fixed": round(rates["early_stop"][0] / rates["fixed"][0], 3),
+              "gpu_launches_per_step": rates["early_stop"][3],
+              "note": "on-device channel + early-stop decode with lane compaction (qc_decode_es) + counters"}
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
@@ -537,6 +568,7 @@ def main():
             "communicator": comm,
             "gpu_launches": eng.kernel_launches_per_step() * args.steps,
             "stream": stream,
+            "early_stop": es,
             "clocks": ck,
             "frame_errors_last_step": int(counts[:, 2].sum()),
         }), flush=True)
