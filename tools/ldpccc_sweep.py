@@ -23,23 +23,37 @@ sys.path.insert(0, REPO)
 
 
 def _cpu_slot_time(args):
+    """Steady-state slot time of the reference's own StreamDecoder (qcldpc from
+    oracle/_ref, unmodified) when installed, else the oracle port."""
     code_name, I, G, seed = args
     import numpy as np
-    from oracle import qc, stream
+    from oracle import build_ref, qc, stream
     import paper_1204_0334_b200 as q
     _, exp = q.load_code(q.codes.bundled_code_path(code_name))
-    U = qc.unwrap(exp.shifts, exp.p)
-    dec = stream.StreamOracle(U, I, G)
-    window = I * (U.ms + 1)
+    if build_ref.available():
+        sys.path.insert(0, build_ref.site_dir())
+        import qcldpc
+        code = qcldpc.unwrap_qc(qcldpc.ExponentMatrix(exp.shifts, exp.p))
+        dec = qcldpc.StreamDecoder(code, I, gamma=G)
+        push, c, window = dec.push_frame, code.c, I * (code.ms + 1)
+    else:
+        U = qc.unwrap(exp.shifts, exp.p)
+        dec = stream.StreamOracle(U, I, G)
+        push, c, window = dec.push, U.c, I * (U.ms + 1)
     rng = np.random.default_rng(seed)
     sigma = 0.55
     for _ in range(window):
-        dec.push(rng.normal(1.0, sigma, size=(G, U.c)), sigma)
+        push(rng.normal(1.0, sigma, size=(G, c)), sigma)
     t0 = time.perf_counter()
     n = 8
     for _ in range(n):
-        dec.push(rng.normal(1.0, sigma, size=(G, U.c)), sigma)
+        push(rng.normal(1.0, sigma, size=(G, c)), sigma)
     return (time.perf_counter() - t0) / n
+
+
+def _ref_available():
+    from oracle import build_ref
+    return build_ref.available()
 
 
 def main():
@@ -93,7 +107,9 @@ def main():
                               "us_per_slot": round(t * 1e6, 1),
                               "steady_mbit_s": round(cores * 32 * b / (t * 1e6), 3),
                               "latency_ms": round(window * t * 1e3, 1),
-                              "impl": "oracle port of StreamDecoder (numpy float64), one decoder per core"}),
+                              "impl": ("qcldpc.StreamDecoder (the reference, unmodified, oracle/_ref)"
+                                       if _ref_available() else "oracle port of StreamDecoder (numpy float64)")
+                                      + ", one decoder per core"}),
                   flush=True)
 
 

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
-synccheck): channel, fused compact decode, two-pass early-stop decode, host
-pipeline with ragged chunks, LDPCCC slots, recycling campaign.
+synccheck / initcheck): channel, fused compact decode, early-stop decodes
+(plain and with lane compaction), host pipeline with ragged chunks, LDPCCC
+slots (public API and look-ahead campaign slots), recycling campaign.
 
   compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
 """
@@ -34,6 +35,20 @@ def main():
     sim = q.SimulationConfig("t", [2.8], iterations=8, gamma=32, stop_block_errors=10**9, max_frames=256,
                              seed=1, early_stop=True)
     q.run_block_simulation(lay, sim, gamma_kernel=128, recycle=True)
+    # round 2: early stop with lane compaction (device engine and host pipeline),
+    # LDPCCC look-ahead slots with batched channel frames
+    ycmp = q.simulate_block(q.ChannelConfig(3.0, 5 / 6, seed=5, gamma=2048), lay.n_vars)
+    r3 = q.decode_batch(lay, ycmp, q.ebn0_to_sigma(3.0, 5 / 6), 24, early_stop=True)   # 1024-lane chunks
+    dec_es = q.BlockDecoder(lay, 1024, 30, early_stop=True, graph=False)
+    assert dec_es.es_scratch is not None
+    dec_es.load_lane_major(ycmp[:1024], q.ebn0_to_sigma(3.0, 5 / 6))
+    dec_es.run()
+    dec_es.result(1024)
+    assert r3.iterations_run.min() < r3.iterations_run.max()
+    scode = q.unwrap_qc(q.multiplicative_shifts(4, 24, 11))
+    scfg = q.SimulationConfig("s", [2.6], iterations=3, gamma=32, stop_block_errors=10**9, max_frames=128,
+                              seed=2, processors=3, stream_segment_frames=12)
+    q.run_stream_simulation(scode, scfg)
     print("sanitize smoke ok")
 
 
