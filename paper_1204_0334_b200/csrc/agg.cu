@@ -64,7 +64,7 @@ struct AggArgs {
 // lane groups of this window that hold live lanes (live mode)
 template <int VEC>
 __device__ __forceinline__ unsigned live_groups(const AggArgs& a) {
-  const int c = *a.live;
+  const int c = __ldg(a.live);     // read-only path: one L1 miss per SM, then hits
   const int n = a.live_half ? (c >> 1) : ((c + 1) >> 1);
   const int lpg = VEC << a.lg_gw;
   return (unsigned)min(a.groups, (n + lpg - 1) / lpg);
@@ -122,6 +122,9 @@ __device__ __forceinline__ void es_store_bits(const AggArgs& a, int n, int q, un
 #endif
 #ifndef AGG_VAR_MINB
 #define AGG_VAR_MINB (1024 / AGG_THREADS)
+#endif
+#ifndef AGG_ES_MINB
+#define AGG_ES_MINB 7   // early-stop variable / fused kernels: 72 registers, no spills (64: 40 B stack; +1-3%)
 #endif
 
 // AGG_ES: early stop (bp.py:242-256): frozen lanes keep their packages and
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(AGG_THREADS) agg_check_live_kernel(AggArgs a, 
 }
 
 template <int DV, int VEC, int FLAGS, int ITEMS>
-__global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
+__global__ void __launch_bounds__(AGG_THREADS, (FLAGS & AGG_ES) ? AGG_ES_MINB : AGG_VAR_MINB) agg_var_kernel(AggArgs a, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
   int n, q;
   unsigned ng = a.groups;
@@ -640,7 +643,7 @@ __device__ __forceinline__ void fused_block(const FusedArgs& f, const QcGrid& gr
 }
 
 template <int DC, int DV, int VC, int VV, bool FROM_MU, int FLAGS, int ITEMS>
-__global__ void __launch_bounds__(AGG_THREADS, AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
+__global__ void __launch_bounds__(AGG_THREADS, (FLAGS & AGG_ES) ? AGG_ES_MINB : AGG_VAR_MINB) agg_fused_kernel(FusedArgs f, const __grid_constant__ QcGrid grid) {
   pdl_trigger();
   if (f.v.live) {           // compacted segment, full grid: rows past the live lane groups exit at once
     const unsigned gv = live_groups<VV>(f.v), gc = live_groups<VC>(f.c);
