@@ -84,6 +84,17 @@ def test_bench_records(gpu):
     recs = q.bench_throughput(lay, toy_cfg(q, ebn0_db=3.0), frames=16)
     assert {r["gamma"] for r in recs} == {1, 8}
     assert all(r["frames"] == 16 and r["mode"] == "block" for r in recs)
+    # workers = concurrent reference batches per launch: the same codewords
+    # decoded with different batching -- identical per-gamma results
+    import multiprocessing
+    cores = multiprocessing.cpu_count()
+    for g in (1, 8):
+        rs = [r for r in recs if r["gamma"] == g]
+        assert {r["workers"] for r in rs} == {1, cores}
+        one = next(r for r in rs if r["workers"] == 1)
+        many = next(r for r in rs if r["workers"] == cores)
+        assert one["batches_per_launch"] == 1
+        assert many["batches_per_launch"] == min(cores, -(-16 // g))
     buf = io.StringIO()
     q.write_jsonl(recs, buf)
     assert [json.loads(l) for l in buf.getvalue().splitlines()] == recs
