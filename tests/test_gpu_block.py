@@ -622,3 +622,26 @@ def test_compacted_early_stop_against_oracle(gpu):
     err = (np.abs(r.posteriors[sel] - post) / np.maximum(np.abs(post), 1.0))[ok]
     assert np.quantile(err, 0.9999) <= 1e-4 and err.max() <= 1e-3, (np.quantile(err, 0.9999), err.max())
     assert len(set(its.tolist())) > 2
+
+
+def test_host_pipeline_compacted_early_stop_equals_plain(gpu):
+    """decode_batch(..., early_stop=True) on 2560 lanes -- 1024-lane chunks
+    through the compacted early-stop decode in the host pipeline, smaller
+    ramp chunks through the plain one -- equals one uncompacted early-stop
+    decode of the whole batch: bits, posteriors, ok, iterations_run."""
+    q = gpu
+    h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
+    lay = q.build_edge_layout(h)
+    G = 2560
+    sigma = q.ebn0_to_sigma(3.2, 1 - lay.n_checks / lay.n_vars)
+    y = q.simulate_block(q.ChannelConfig(3.2, 1 - lay.n_checks / lay.n_vars, seed=8, gamma=G), lay.n_vars)
+    r = q.decode_batch(lay, y, sigma, 30, early_stop=True)
+    dec = q.BlockDecoder(lay, G, 30, early_stop=True, graph=False, compact=False)
+    dec.load_lane_major(y, sigma)
+    dec.run()
+    ref = dec.result(G)
+    assert np.array_equal(r.iterations_run, ref.iterations_run)
+    assert np.array_equal(r.syndrome_ok, ref.syndrome_ok)
+    assert np.array_equal(r.hard_bits, ref.hard_bits)
+    assert np.array_equal(r.posteriors, ref.posteriors)
+    assert r.iterations_run.min() < 12 < r.iterations_run.max()
