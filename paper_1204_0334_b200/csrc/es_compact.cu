@@ -44,10 +44,11 @@ constexpr int CK_THREADS = 1024;
 constexpr int MAX_CHECKPOINTS = 6;
 
 // checkpoint iterations (after these, the continuing lanes are packed); chosen
-// from the iteration histogram of n18360 at 3.0-3.6 dB
-// (profiles/r02/iters_hist.jsonl): 10 -> 62% of lanes still iterating at
-// 3.2 dB, 13 -> 19%, 17 -> 4%, 22 -> 1.4%
-constexpr int CHECKPOINTS[] = {10, 13, 17, 22};
+// from the iteration histogram of n18360 (profiles/r02/iters_hist.jsonl: at
+// 3.2 dB 43% of lanes still iterate after 11, 12% after 14, 3% after 18) and an
+// A/B of five schedules (kbench_ck.jsonl): three checkpoints beat four or five
+// in the waterfall (3.0-3.2 dB, 4%), earlier / more ones win only above it
+constexpr int CHECKPOINTS[] = {11, 14, 18};
 
 struct CkArgs {
   // state of the current set after its last variable pass at iteration c
