@@ -123,6 +123,7 @@ class StreamDecoder:
         self._ev_rest = None     # end of the last slot's main-stream work
         self._kind = np.zeros((processors, code.lam * code.lam), dtype=np.int8)
         self._ring_live = np.zeros(self.window, dtype=bool)
+        self._tracked = 0          # slots folded into _kind / _ring_live (brought up to date on access)
 
     # What each (processor group, sub-block label) block of the message store
     # holds in the REFERENCE's terms after the slots run so far (host-side
@@ -130,6 +131,14 @@ class StreamDecoder:
     # keeps var->check messages in phi form and skips the emission-time clear
     # (convolutional.py:328-330), so message_memory / channel_memory translate.
     _ZERO, _BETA, _ALPHA = 0, 1, 2
+
+    def _sync_track(self):
+        """Bring the block-kind / ring-liveness tables up to slot self.t -- done
+        when message_memory / channel_memory are read, not on every push (the
+        per-slot bookkeeping is ~I*T table writes of host Python)."""
+        for t in range(self._tracked, self.t):
+            self._track(t)
+        self._tracked = self.t
 
     def _track(self, t):
         code, T, I, kind = self.code, self.period, self.processors, self._kind
@@ -160,6 +169,7 @@ class StreamDecoder:
         emitted frames read 0.0 as in the reference (convolutional.py:331)."""
         import torch
         torch.cuda.synchronize()
+        self._sync_track()
         ring = self._ring[:, :, : self.gamma].double().cpu().numpy()
         ring[~self._ring_live] = 0.0
         return ring
@@ -173,6 +183,7 @@ class StreamDecoder:
         rounding), 0.0 on never-written / emitted blocks."""
         import torch
         torch.cuda.synchronize()
+        self._sync_track()
         code = self.code
         m = self._msg[:, : self.gamma].double().cpu().numpy()
         m = m.reshape(self.processors, code.edge_count, self.gamma)
@@ -288,7 +299,6 @@ class StreamDecoder:
         processors 0..I-2 (the whole slot when nothing was split off)."""
         import torch
         t = self.t
-        self._track(t)
         I = self.processors
         j = t - self.window + 1
         post = self._post.data_ptr() if (j >= 0 and not split) else None
