@@ -155,8 +155,12 @@ __global__ void __launch_bounds__(CK_THREADS) es_ckpt_kernel(CkArgs a) {
 
 // done lanes of a compacted set -> the caller's arrays by original id
 // (cont == null: every mapped lane, the final segment)
-__global__ void es_scatter_kernel(const float* post_s, const uint8_t* ok_s, const int32_t* it_s, const int32_t* map,
-                                  const uint32_t* cont, float* post_out, uint8_t* ok_out, int32_t* it_out, int N,
+#ifndef ES_ROWS
+#define ES_ROWS 8   // rows per pass of the gather / scatter copies (loads in flight per thread)
+#endif
+
+__global__ void es_scatter_kernel(const float* __restrict__ post_s, const uint8_t* ok_s, const int32_t* it_s, const int32_t* map,
+                                  const uint32_t* cont, float* __restrict__ post_out, uint8_t* ok_out, int32_t* it_out, int N,
                                   int gamma) {
   const int pl = blockIdx.x * blockDim.x + threadIdx.x;
   if (pl >= gamma) return;
@@ -167,19 +171,42 @@ __global__ void es_scatter_kernel(const float* post_s, const uint8_t* ok_s, cons
     ok_out[m] = ok_s[pl];
     it_out[m] = it_s[pl];
   }
-  for (int n = blockIdx.y; n < N; n += gridDim.y) post_out[(size_t)n * gamma + m] = post_s[(size_t)n * gamma + pl];
+  // ES_ROWS rows per pass: their loads are all in flight before the stores
+  const int step = gridDim.y;
+  int n = blockIdx.y;
+  for (; n + (ES_ROWS - 1) * step < N; n += ES_ROWS * step) {
+    float v[ES_ROWS];
+#pragma unroll
+    for (int k = 0; k < ES_ROWS; ++k) v[k] = post_s[(size_t)(n + k * step) * gamma + pl];
+#pragma unroll
+    for (int k = 0; k < ES_ROWS; ++k) post_out[(size_t)(n + k * step) * gamma + m] = v[k];
+  }
+  for (; n < N; n += step) post_out[(size_t)n * gamma + m] = post_s[(size_t)n * gamma + pl];
 }
 
 // continuing lanes' packages (rows [0, E)) and LLRs (rows [E, E + N)) into the next set
-__global__ void es_gather_kernel(const float* msgs_s, float* msgs_d, const float* mu_s, float* mu_d,
-                                 const int32_t* src, const int32_t* count, int E, int N, int gamma, int H) {
+__device__ __forceinline__ void gather_rows(const float* __restrict__ src_rows, float* __restrict__ dst_rows,
+                                            int rows, int gamma, int sp, int dp) {
+  const int step = gridDim.y;
+  int r = blockIdx.y;
+  for (; r + (ES_ROWS - 1) * step < rows; r += ES_ROWS * step) {
+    float v[ES_ROWS];
+#pragma unroll
+    for (int k = 0; k < ES_ROWS; ++k) v[k] = src_rows[(size_t)(r + k * step) * gamma + sp];
+#pragma unroll
+    for (int k = 0; k < ES_ROWS; ++k) dst_rows[(size_t)(r + k * step) * gamma + dp] = v[k];
+  }
+  for (; r < rows; r += step) dst_rows[(size_t)r * gamma + dp] = src_rows[(size_t)r * gamma + sp];
+}
+
+__global__ void es_gather_kernel(const float* __restrict__ msgs_s, float* __restrict__ msgs_d,
+                                 const float* __restrict__ mu_s, float* __restrict__ mu_d, const int32_t* src,
+                                 const int32_t* count, int E, int N, int gamma, int H) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *count) return;
   const int sp = src[i], dp = (i & 1) * H + (i >> 1);
-  for (int r = blockIdx.y; r < E + N; r += gridDim.y) {
-    if (r < E) msgs_d[(size_t)r * gamma + dp] = msgs_s[(size_t)r * gamma + sp];
-    else mu_d[(size_t)(r - E) * gamma + dp] = mu_s[(size_t)(r - E) * gamma + sp];
-  }
+  gather_rows(msgs_s, msgs_d, E, gamma, sp, dp);
+  gather_rows(mu_s, mu_d, N, gamma, sp, dp);
 }
 
 struct Set {
