@@ -225,11 +225,13 @@ __global__ void __launch_bounds__(CC_THREADS) entry_kernel(SlotArgs a, const __g
   pdl_trigger();
   pdl_wait();
   const int t = slot_of(a);
-  const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int T = TT ? TT : P.lam;
+  const unsigned GV = (unsigned)P.gamma / VEC;
+  // 32-bit index math (the launchers keep the thread count < 2^31)
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
   fold_prev(a, P, t, P.I * T, tid);
-  if (tid >= (long long)P.c * GV) return;
-  const int v = (int)(tid / GV), q = (int)(tid - (long long)v * GV);
+  if (tid >= (unsigned)P.c * GV) return;
+  const int v = (int)(tid / GV), q = (int)(tid - (unsigned)v * GV);
   entry_body<DV, VEC, QC, TT, SJ>(a, P, t, a.mu_in, v, q);
 }
 
@@ -241,14 +243,15 @@ __global__ void __launch_bounds__(CC_THREADS) check_kernel(SlotArgs a, const __g
   pdl_trigger();
   pdl_wait();
   const int t = slot_of(a);
-  const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int T = TT ? TT : P.lam;
+  const unsigned GV = (unsigned)P.gamma / VEC, per = (unsigned)P.cb * GV;
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (a.fold_in_check) fold_prev(a, P, t, P.I * T, tid);
-  if (tid >= (long long)a.nip * P.cb * GV) return;
-  const int ipl = (int)(tid / ((long long)P.cb * GV));
-  const int ip = a.ip0 + ipl;
-  int rem = (int)(tid - (long long)ipl * P.cb * GV);
-  int r = rem / GV, q = rem - r * GV;
+  if (tid >= (unsigned)a.nip * per) return;
+  const unsigned ipl = tid / per;
+  const int ip = a.ip0 + (int)ipl;
+  const unsigned rem = tid - ipl * per;
+  const int r = (int)(rem / GV), q = (int)(rem - (unsigned)r * GV);
   const int s = t - ip * T;
   if (s < 0) return;
   const int kap = pmod(s, T);
@@ -337,13 +340,14 @@ __global__ void __launch_bounds__(CC_THREADS) var_kernel(SlotArgs a, const __gri
   pdl_trigger();
   pdl_wait();
   const int t = slot_of(a);
-  const int T = TT ? TT : P.lam, GV = P.gamma / VEC;
-  long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)a.nip * P.c * GV) return;
-  const int ipl = (int)(tid / ((long long)P.c * GV));
-  const int ip = a.ip0 + ipl;
-  int rem = (int)(tid - (long long)ipl * P.c * GV);
-  int v = rem / GV, q = rem - v * GV;
+  const int T = TT ? TT : P.lam;
+  const unsigned GV = (unsigned)P.gamma / VEC, per = (unsigned)P.c * GV;
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (unsigned)a.nip * per) return;
+  const unsigned ipl = tid / per;
+  const int ip = a.ip0 + (int)ipl;
+  const unsigned rem = tid - ipl * per;
+  const int v = (int)(rem / GV), q = (int)(rem - (unsigned)v * GV);
   const int j = t - (ip + 1) * T + 1;
   const bool enter = a.entry_next && ip + 1 == P.I;   // look-ahead entry of frame t + 1 (= j + window)
   if (j < 0) {
@@ -430,12 +434,21 @@ CcParams make_params(const cc_plan* pl, int I, int gamma) {
   return P;
 }
 
-// lanes per thread: check pass float2 (register-heavy), entry / variable float4
+// lanes per thread: check pass float2 (register-heavy), entry / variable float4.
+// From 8 lane vectors per row (gamma 32: a warp spans 4 variables' rows of
+// 128 B): the per-thread index math (slot / processor / node decomposition,
+// edge walk) is shared by VEC lanes, which is what bounds small-gamma slots
+// (ncu at gamma 32, one lane per thread: 80% issue slots, 24% IMAD).
+#ifndef CC_MIN_GV
+#define CC_MIN_GV 8
+#endif
 inline int vec_for(int gamma, int want) {
-  if (want >= 4 && gamma % 128 == 0) return 4;
-  if (want >= 2 && gamma % 64 == 0) return 2;
+  if (want >= 4 && gamma % 4 == 0 && gamma / 4 >= CC_MIN_GV) return 4;
+  if (want >= 2 && gamma % 2 == 0 && gamma / 2 >= CC_MIN_GV) return 2;
   return 1;
 }
+
+inline bool fits32(long long threads) { return threads < (1ll << 31) - CC_THREADS; }
 
 template <int DV, bool QC, int TT = 0, int SJ = 0>
 void launch_entry(const CcParams& P, const SlotArgs& a, cudaStream_t s) {
@@ -617,6 +630,7 @@ int cc_slot_part(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t* 
   if (t > 0x3fffffff || t < -0x3fffffff) return fail_arg("slot index out of range");
   if (ip0 < 0 || nip < 0 || ip0 + nip > I || parts < 0 || parts > SLOT_ALL)
     return fail_arg("processor range / parts out of range");
+  if (!fits32((long long)I * std::max(pl->c, pl->cb) * gamma)) return fail_arg("I x nodes x gamma too large for one launch");
   if (parts == 0 || (nip == 0 && !(parts & SLOT_ENTRY))) return 0;
   cudaStream_t s = as_stream(stream);
   CcParams P = make_params(pl, I, gamma);
@@ -643,6 +657,7 @@ int cc_slot_ahead(const cc_plan* pl, int I, int gamma, int64_t t, const int64_t*
   if (gamma <= 0 || gamma % 32) return fail_arg("gamma must be a positive multiple of 32");
   if (!t_dev && t < 0) return fail_arg("slot index must be non-negative");
   if (t > 0x3fffffff || t < -0x3fffffff) return fail_arg("slot index out of range");
+  if (!fits32((long long)I * std::max(pl->c, pl->cb) * gamma)) return fail_arg("I x nodes x gamma too large for one launch");
   cudaStream_t s = as_stream(stream);
   CcParams P = make_params(pl, I, gamma);
   SlotArgs a{msg, ring, nullptr, post_out, lane_cnt, pl->d_check_tab, pl->d_var_tab, t_dev, (int)t, 0, I,
