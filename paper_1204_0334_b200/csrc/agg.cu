@@ -709,13 +709,45 @@ constexpr int AGG_FVC = 4;            // lanes per thread of the fused check job
 bool dc_supported(int dc) { return dc == 4 || dc == 6 || dc == 8 || dc == 12 || dc == 16 || dc == 24 || dc == 32; }
 bool dv_supported(int dv) { return dv >= 2 && dv <= 4; }
 
+int pick_lg_gw(int gamma, int vec);
 int pick_vec(int gamma) { return gamma % 128 == 0 ? 4 : (gamma % 64 == 0 ? 2 : 1); }
+
+// Small batches (gamma < 128) on the fixed-iteration passes: up to `want` lanes
+// per thread from AGG_MIN_GV lane vectors per row (gamma 32: a warp spans 2
+// rows), so the per-thread index math and record gathers are shared by several
+// lanes -- the LDPCCC slots' fix for the same bound (stream.cu, vec_for).  The
+// hard-bit shuffles then run over 32 / VEC-thread groups of one row: rows whose
+// warps are partially out of range would leave the full-warp shuffle short, so
+// the variable pass takes it only when the row count divides evenly.
+#ifndef AGG_MIN_GV
+#define AGG_MIN_GV 16      // gamma 32: 2 lanes per thread (2 rows per warp) beat 4 (4 rows per warp)
+#endif
+#ifndef AGG_SMALL_VC
+#define AGG_SMALL_VC 4     // lanes per thread, small-batch check pass
+#endif
+#ifndef AGG_SMALL_VV
+#define AGG_SMALL_VV 4     // lanes per thread, small-batch variable pass
+#endif
+int pick_vec_small(int lanes, int want, int rows) {
+  for (int v = want; v > 1; v >>= 1) {
+    const int gv = lanes / v;
+    if (lanes % v || gv < AGG_MIN_GV || (gv >= 32 && gv % 32)) continue;   // lane groups must tile the row
+    const int rows_per_warp = 32 / std::min(32, 1 << pick_lg_gw(lanes, v));
+    if (rows % rows_per_warp == 0) return v;
+  }
+  return 1;
+}
 int pick_vec_var(int gamma) { return std::min(pick_vec(gamma), AGG_VV); }
 
 // log2 of the lane vectors per group: the largest power of two <= LG/VEC that
 // divides GV = gamma/VEC (GV is a multiple of 32 for every vec pick_vec returns)
 int pick_lg_gw(int gamma, int vec) {
   int GV = gamma / vec, target = std::max(32, AGG_LANE_GROUP / vec), lg = 5;
+  if (GV < 32) {              // small batches (pick_vec_small): several rows per warp
+    lg = 0;
+    while (GV % (2 << lg) == 0 && (2 << lg) <= GV) ++lg;
+    return lg;
+  }
   while ((2 << lg) <= target && GV % (2 << lg) == 0) ++lg;
   return lg;
 }
@@ -923,7 +955,8 @@ int launch_agg_check(const qc_plan* p, int gamma, bool from_mu, float* msgs, con
 int launch_agg_check_w(const qc_plan* p, int gamma, int lane0, int lanes, bool from_mu, float* msgs,
                        const float* mu, float* agg, cudaStream_t s, const uint32_t* active, const int32_t* live,
                        int live_loop) {
-  const int vec = pick_vec(lanes);
+  int vec = pick_vec(lanes);
+  if (lanes < 128 && !active && !live) vec = std::max(vec, pick_vec_small(lanes, AGG_SMALL_VC, p->M));
   AggArgs a = make_args(msgs, mu, agg, nullptr, nullptr, p->M, gamma, lane0, lanes, vec, 0);
   a.active = active;
   a.live = live;
@@ -951,7 +984,8 @@ int launch_agg_var(const qc_plan* p, int gamma, int flags, float* msgs, const fl
 int launch_agg_var_w(const qc_plan* p, int gamma, int lane0, int lanes, int flags, float* msgs, const float* mu,
                      const float* agg, float* post, uint32_t* hb, cudaStream_t s, const uint32_t* active,
                      const uint32_t* active2, const int32_t* live, int live_loop) {
-  const int vec = pick_vec_var(lanes);
+  int vec = pick_vec_var(lanes);
+  if (lanes < 128 && !(flags & AGG_ES) && !active && !live) vec = std::max(vec, pick_vec_small(lanes, AGG_SMALL_VV, p->N));
   AggArgs a = make_args(msgs, mu, const_cast<float*>(agg), post, hb, p->N, gamma, lane0, lanes, vec,
                         AGG_REVERSE);
   a.active = active;

@@ -449,6 +449,45 @@ def test_compact_schedule_decode_is_bit_identical(gpu, tmp_path):
             assert np.array_equal(outs[0], o), gamma
 
 
+_SMALL_SNIPPET = r"""
+import sys, numpy as np
+import paper_1204_0334_b200 as q
+out = {}
+for name in ("toy", "n18360"):
+    if name == "toy":
+        lay = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
+    else:
+        lay = q.build_edge_layout(q.load_code(q.codes.bundled_code_path("n18360"))[0])
+    for gamma in (32, 64, 96):
+        y = np.random.default_rng(gamma).normal(1.0, 0.8, size=(gamma, lay.n_vars))
+        dec = q.BlockDecoder(lay, gamma, 12, early_stop=False, graph=False)
+        dec.load_lane_major(y, 0.8)
+        dec.run()
+        r = dec.result(gamma)
+        out[f"{name}{gamma}p"] = r.posteriors
+        out[f"{name}{gamma}b"] = r.hard_bits
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_small_batch_passes_are_bit_identical(gpu, tmp_path):
+    """Batches below 128 lanes run the compact passes with several lanes per
+    thread from 8 lane vectors per row (agg.cu pick_vec_small: gamma 32 -> 4
+    rows per warp); decisions and posteriors equal the two-pass reference
+    schedule (QCB_AGG=0) bit for bit, including gamma 96 (3 lane groups)."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({"QCB_AGG": "0"}, {"QCB_AGG": "1"}):
+        f = tmp_path / f"small_{len(outs)}.npz"
+        subprocess.run([sys.executable, "-c", _SMALL_SNIPPET, str(f)], cwd=repo, check=True, env={**os.environ, **env})
+        outs.append(dict(np.load(f)))
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
 def rel_err(got, ref, atol=1e-12):
     """|delta| / (|ref| + atol): the north star's relative measure (atol only
     guards exact zeros of the reference; fp32 cannot represent below ~1e-38)."""
