@@ -275,11 +275,20 @@ __global__ void __launch_bounds__(THREADS) vnu_kernel(VnuArgs a, const __grid_co
 
 // check pass: 2 lanes per thread (float2) -- measured best on B200 at d_c = 24
 // (4 lanes: 171 registers, 8 warps/SM; 1 lane: LSU-issue bound)
-inline int pick_vec_cnu(int gamma, int) { return gamma % 64 == 0 ? 2 : 1; }
+// Small batches (the two-pass early stop at gamma < 128): lanes per thread up
+// to 16 lane vectors per row, so the per-thread index math is shared (gamma
+// 32: 2 lanes, two rows per warp; the hard-bit shuffle groups of 32 / VEC
+// threads still cover one row's 32-lane word).
+inline int pick_vec_cnu(int gamma, int) {
+  if (gamma % 64 == 0) return 2;
+  return (gamma % 2 == 0 && gamma / 2 >= 16) ? 2 : 1;
+}
 // variable pass: float4 packages
 inline int pick_vec_vnu(int gamma) {
   if (gamma % 128 == 0) return 4;
-  return gamma % 64 == 0 ? 2 : 1;
+  if (gamma % 4 == 0 && gamma / 4 >= 16) return 4;
+  if (gamma % 2 == 0 && gamma / 2 >= 16) return 2;
+  return 1;
 }
 
 QcGrid make_grid(const qc_plan* p);
