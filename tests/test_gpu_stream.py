@@ -75,9 +75,12 @@ def test_stream_lanes_independent_and_gamma_invariant(gpu):
         single = {f.frame_index: f for f in run(q, code, 2, 1, ys[:, lane:lane + 1], 1.0)}
         for j in range(12):
             assert np.array_equal(wide[j].posteriors[lane], single[j].posteriors[0])
-    big = {f.frame_index: f for f in run(q, code, 2, 130, np.repeat(ys[:, :1], 130, axis=1), 1.0)}
-    for j in range(12):
-        assert np.array_equal(big[j].posteriors, np.repeat(wide[j].posteriors[:1], 130, axis=0))
+    # padded widths 64, 96, 160: 4 / 2 lanes per thread with 16, 24, 40 lane
+    # vectors per row (stream.cu vec_for) -- same bits as the 32-lane run
+    for G in (50, 96, 130):
+        big = {f.frame_index: f for f in run(q, code, 2, G, np.repeat(ys[:, :1], G, axis=1), 1.0)}
+        for j in range(12):
+            assert np.array_equal(big[j].posteriors, np.repeat(wide[j].posteriors[:1], G, axis=0)), G
 
 
 def test_stream_api_contract(gpu):
