@@ -27,6 +27,13 @@ def main():
     assert r.hard_bits.shape == y.shape and r2.iterations_run.max() <= 6
     toy = q.build_edge_layout(q.expand_qc(q.multiplicative_shifts(2, 4, 8)))
     q.decode_batch(toy, np.random.default_rng(1).normal(1, 0.8, (70, toy.n_vars)), 0.8, 5)
+    # small batches: several rows per warp (block passes 2 / 4 lanes per thread)
+    for G, es in ((32, False), (64, False), (32, True)):
+        q.decode_batch(lay, y[:G], cfg.sigma, 5, early_stop=es)
+    d96 = q.BlockDecoder(lay, 96, 5, early_stop=False, graph=False)
+    d96.load_lane_major(y[:96], cfg.sigma)
+    d96.run()
+    d96.result(96)
     code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 11))
     dec = q.StreamDecoder(code, 2, gamma=3)
     for t in range(12):
