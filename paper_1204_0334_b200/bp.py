@@ -365,6 +365,9 @@ HOST_CHUNK_ES = 1024    # chunk of early-stop batches from 2048 lanes (lane comp
 HOST_SLOTS = 4          # CUDA streams (device buffer sets) the chunks rotate over, pageable input
 HOST_SLOTS_PINNED = 3   # same for page-locked input (no host staging copy to hide; tools/e2e_bench.py)
 PINNED_MIN_BYTES = 1 << 20
+# pageable inputs up to this size are staged page-locked in one copy (1.1-1.7x
+# at 32-1024 lanes of n18360; above it the pipeline's fp32 staging threads win)
+STAGE_PAGEABLE_MAX_BYTES = 160 << 20
 
 
 class HostDecoder:
@@ -445,14 +448,20 @@ def host_array(a: np.ndarray) -> np.ndarray:
 def _host_decoder(layout: EdgeLayout, gamma: int, iterations: int, early_stop: bool,
                   pinned_input: bool = False) -> HostDecoder:
     import torch
-    # small batches: one chunk rounded up to a multiple of 64 lanes; from 256
-    # lanes up at least two chunks, so the copy-in of one overlaps the decode of
-    # another (e.g. 512 lanes: 64 + 128 + 256 + 64 over chunk 256, 1.6x the
-    # single-chunk rate; profiles/r02/e2e_gamma_curve.md)
+    # small batches: one chunk up to 64 lanes; above that at least two chunks,
+    # so the copy-in of one overlaps the decode of another: 64-lane chunks up to
+    # 128 lanes, 128-lane chunks below 256 (96 / 128 / 160 / 192 lanes: 15-25%
+    # faster than one chunk since the small-batch passes got cheaper,
+    # profiles/r02/e2e_chunk_sweep.jsonl); from 256 lanes about two chunks
+    # (e.g. 512 lanes: 64 + 128 + 256 + 64 over chunk 256)
     if gamma <= 32:
         chunk = pad32(gamma)
+    elif gamma <= 64:
+        chunk = 64
+    elif gamma <= 128:
+        chunk = 64
     elif gamma < 256:
-        chunk = (gamma + 63) // 64 * 64
+        chunk = 128
     else:
         chunk = min(HOST_CHUNK, max(128, ((gamma + 1) // 2 + 63) // 64 * 64))
     if early_stop and gamma >= 2 * HOST_CHUNK_ES:
@@ -496,6 +505,15 @@ def _decode_host(layout: EdgeLayout, x: np.ndarray, sigma: float | None, iterati
             return dec.result(x.shape[0])
     x = np.ascontiguousarray(x, dtype=np.float64)
     pinned = bool(x.size) and _lib.load().qc_host_is_pinned(x.ctypes.data, x.nbytes) == 1
+    if not pinned and 0 < x.nbytes <= STAGE_PAGEABLE_MAX_BYTES:
+        # ordinary numpy input of a small batch: one multi-threaded copy into
+        # page-locked memory (torch's intra-op pool, no thread start-up) and the
+        # page-locked path, instead of the pipeline's per-call staging threads
+        # (profiles/r02/e2e_pageable_small.jsonl)
+        import torch
+        staged = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
+        staged.copy_(torch.from_numpy(x))
+        x, pinned = staged.numpy(), True
     return _host_decoder(layout, x.shape[0], iterations, early_stop, pinned).decode(x, sigma or 0.0)
 
 
