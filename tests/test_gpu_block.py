@@ -260,6 +260,7 @@ def test_pageable_llr_staging_matches_pinned(gpu, monkeypatch):
     q = gpu
     from paper_1204_0334_b200 import bp as qbp
     monkeypatch.setattr(qbp, "HOST_CHUNK", 64)
+    monkeypatch.setattr(qbp, "STAGE_PAGEABLE_MAX_BYTES", 0)   # keep the native pageable staging in play
     lay = toy(q)
     rng = np.random.default_rng(9)
     sigma = 0.7
