@@ -142,6 +142,15 @@ QC_API int qc_lane_major(int n, int gamma, int gamma_out, const float* post, dou
 /* same with an fp32 posterior output (half the device->host bytes) */
 QC_API int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post, float* post_out,
                              uint8_t* bits_out, void* stream);
+/* host-array forms (StreamDecoder.push_frame, convolutional.py:220-246): the
+ * lane-major conversion into device staging (post_dev, bits_dev) followed by
+ * asynchronous copies to the host arrays (page-locked for true asynchrony); and
+ * an asynchronous copy of lane-major host values into x_dev followed by
+ * qc_llr_from_lane_major.  Stream-ordered; the caller synchronises. */
+QC_API int qc_lane_major_to_host(int n, int gamma, int gamma_out, const float* post, double* post_dev,
+                                 uint8_t* bits_dev, double* post_host, uint8_t* bits_host, void* stream);
+QC_API int qc_llr_from_host(int n, int gamma, int gamma_in, const double* x_host, double* x_dev, double sigma,
+                            float* mu_vm, void* stream);
 /* lane-major fp64 -> variable-major fp32 LLRs, lanes >= gamma_in padded with +50:
  * sigma > 0: x are received values, mu = clip((2 x)/(sigma sigma), +-50) (channel_llrs, bp.py:54-56);
  * sigma <= 0: x are LLRs, mu = clip(x, +-50) (decode_llr_batch, bp.py:231). */

@@ -47,6 +47,8 @@ SIGNATURES = {
     "qc_agg_var": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p]),
     "qc_agg_fused": (_i, [_p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p]),
     "qc_decode_launches": (_i, [_p, _i, _i, _i]),
+    "qc_lane_major_to_host": (_i, [_i, _i, _i, _p, _p, _p, _p, _p, _p]),
+    "qc_llr_from_host": (_i, [_i, _i, _i, _p, _p, _d, _p, _p]),
     "qc_lane_major": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_lane_major_f32": (_i, [_i, _i, _i, _p, _p, _p, _p]),
     "qc_llr_from_lane_major": (_i, [_i, _i, _i, _p, _d, _p, _p]),
@@ -129,5 +131,10 @@ def ptr(t) -> int | None:
 
 
 def stream_handle(device=None) -> int:
+    """cudaStream_t of torch's current stream (on `device`, default the current
+    device) -- the raw-stream query, without torch.cuda.current_stream()'s
+    per-call device resolution (~13 us, a third of a small push_frame)."""
     import torch
+    if device is None:
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
     return torch.cuda.current_stream(device).cuda_stream

@@ -424,13 +424,14 @@ def release_pinned_cache() -> None:
     torch._C._host_emptyCache()
 
 
-def host_empty(shape, dtype) -> np.ndarray:
+def host_empty(shape, dtype, min_bytes: int | None = None) -> np.ndarray:
     """Output array for the host-buffer API: large ones come from torch's caching
     page-locked allocator (unless set_pinned_outputs(False)), so the decoder
     DMAs straight into them and a freed result's pages are reused by the next
     call (no fresh page faults)."""
     dtype = np.dtype(dtype)
-    if not _PINNED_OUTPUTS[0] or int(np.prod(shape)) * dtype.itemsize < PINNED_MIN_BYTES:
+    floor = PINNED_MIN_BYTES if min_bytes is None else min_bytes
+    if not _PINNED_OUTPUTS[0] or int(np.prod(shape)) * dtype.itemsize < floor:
         return np.empty(shape, dtype=dtype)
     import torch
     tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,

@@ -217,19 +217,20 @@ class StreamDecoder:
             raise ValueError(f"expected frame shape {(self.gamma, self.code.c)}, got {y.shape}")
         import torch
         em = self._emit_begin()
-        # page-locked staging: the host copy and an asynchronous H2D
+        # page-locked staging (torch's multi-threaded host copy), then one call:
+        # asynchronous H2D + LLR conversion on the current stream
         if self._y_host is None:
             self._y_host = torch.empty((self.gamma, self.code.c), dtype=torch.float64, pin_memory=True)
             self._y_ev = torch.cuda.Event()
         else:
             self._y_ev.synchronize()     # the previous frame's copy has left the staging buffer
         self._y_host.copy_(torch.from_numpy(np.ascontiguousarray(y)))
-        self._y.copy_(self._y_host, non_blocking=True)
-        self._y_ev.record()
         s = abs(float(sigma))
-        _lib.call("qc_llr_from_lane_major", self.code.c, self._gp, self.gamma, self._y.data_ptr(),
-                  s if s > 0.0 else 1e-300, self._mu.data_ptr(), _lib.stream_handle())
-        self._rest(self._mu, em is not None)
+        st = _lib.stream_handle()
+        _lib.call("qc_llr_from_host", self.code.c, self._gp, self.gamma, self._y_host.data_ptr(), self._y.data_ptr(),
+                  s if s > 0.0 else 1e-300, self._mu.data_ptr(), st)
+        self._y_ev.record()
+        self._rest(self._mu, em is not None, st)
         return self._emit_end(em, tail=False)
 
     def push_llr_device(self, mu_dev) -> DecodedFrame | None:
@@ -272,6 +273,7 @@ class StreamDecoder:
         from .bp import host_empty
         if self._es is None:
             self._es = torch.cuda.Stream()
+            self._es_ev = torch.cuda.Event()
             self._lm = (torch.empty((self.gamma, self.code.c), dtype=torch.float64, device=self._post.device),
                         torch.empty((self.gamma, self.code.c), dtype=torch.uint8, device=self._post.device))
         es = self._es
@@ -282,19 +284,18 @@ class StreamDecoder:
         c, I = self.code.c, self.processors
         _lib.call("cc_slot_part", self._plan.handle, I, self._gp, t, None, self._msg.data_ptr(),
                   self._ring.data_ptr(), None, self._post.data_ptr(), None, I - 1, 1, 6, es.cuda_stream)
+        # page-locked outputs whatever their size: a copy into pageable memory
+        # would block this call until the emitting chain finished
+        post = host_empty((self.gamma, c), np.float64, min_bytes=0)
+        bits = host_empty((self.gamma, c), np.uint8, min_bytes=0)
         post_d, bits_d = self._lm
-        _lib.call("qc_lane_major", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
-                  bits_d.data_ptr(), es.cuda_stream)
-        post = host_empty((self.gamma, c), np.float64)
-        bits = host_empty((self.gamma, c), np.uint8)
-        with torch.cuda.stream(es):
-            torch.from_numpy(post).copy_(post_d, non_blocking=True)
-            torch.from_numpy(bits).copy_(bits_d, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
+        _lib.call("qc_lane_major_to_host", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
+                  bits_d.data_ptr(), post.ctypes.data, bits.ctypes.data, es.cuda_stream)
+        ev = self._es_ev                          # recorded and waited for within this push
+        ev.record(es)
         return j, post, bits, ev
 
-    def _rest(self, mu_dev, split: bool):
+    def _rest(self, mu_dev, split: bool, stream=None):
         """Queue the rest of slot t on the main stream: the entry of frame t and
         processors 0..I-2 (the whole slot when nothing was split off)."""
         import torch
@@ -304,7 +305,7 @@ class StreamDecoder:
         post = self._post.data_ptr() if (j >= 0 and not split) else None
         _lib.call("cc_slot_part", self._plan.handle, I, self._gp, t, None, self._msg.data_ptr(),
                   self._ring.data_ptr(), _lib.ptr(mu_dev), post, None, 0, I - 1 if split else I, 7,
-                  _lib.stream_handle())
+                  stream if stream is not None else _lib.stream_handle())
         if self._ev_rest is None:
             self._ev_rest = torch.cuda.Event()
         self._ev_rest.record()
@@ -328,11 +329,9 @@ class StreamDecoder:
             self._lm = (torch.empty((self.gamma, c), dtype=torch.float64, device=self._post.device),
                         torch.empty((self.gamma, c), dtype=torch.uint8, device=self._post.device))
         post_d, bits_d = self._lm
-        _lib.call("qc_lane_major", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
-                  bits_d.data_ptr(), _lib.stream_handle())
-        post = host_empty((self.gamma, c), np.float64)
-        bits = host_empty((self.gamma, c), np.uint8)
-        torch.from_numpy(post).copy_(post_d, non_blocking=True)
-        torch.from_numpy(bits).copy_(bits_d, non_blocking=True)
+        post = host_empty((self.gamma, c), np.float64, min_bytes=0)
+        bits = host_empty((self.gamma, c), np.uint8, min_bytes=0)
+        _lib.call("qc_lane_major_to_host", c, self._gp, self.gamma, self._post.data_ptr(), post_d.data_ptr(),
+                  bits_d.data_ptr(), post.ctypes.data, bits.ctypes.data, _lib.stream_handle())
         torch.cuda.current_stream().synchronize()
         return DecodedFrame(frame_index=j, hard_bits=bits, posteriors=post, tail=tail)

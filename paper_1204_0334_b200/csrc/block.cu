@@ -508,6 +508,38 @@ int qc_lane_major_f32(int n, int gamma, int gamma_out, const float* post, float*
   return check_launch("lane_major_f32");
 }
 
+// host-array forms for per-frame I/O (StreamDecoder.push_frame): one C call
+// instead of a torch copy + kernel call per direction (per-push host overhead
+// dominates small-gamma pushes, profiles/r02/stream_api_push_frame.md)
+int qc_lane_major_to_host(int n, int gamma, int gamma_out, const float* post, double* post_dev,
+                          uint8_t* bits_dev, double* post_host, uint8_t* bits_host, void* stream) {
+  if ((post_host && !post_dev) || (bits_host && !bits_dev)) return fail_arg("device staging missing");
+  if (int r = qc_lane_major(n, gamma, gamma_out, post, post_dev, bits_dev, stream)) return r;
+  cudaStream_t s = as_stream(stream);
+  const size_t cnt = (size_t)n * gamma_out;
+  if (post_host && cnt) {
+    cudaError_t e = cudaMemcpyAsync(post_host, post_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return fail_rt(std::string("lane_major_to_host: ") + cudaGetErrorString(e));
+  }
+  if (bits_host && cnt) {
+    cudaError_t e = cudaMemcpyAsync(bits_host, bits_dev, cnt, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return fail_rt(std::string("lane_major_to_host: ") + cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+int qc_llr_from_host(int n, int gamma, int gamma_in, const double* x_host, double* x_dev, double sigma,
+                     float* mu_vm, void* stream) {
+  if (!x_host || !x_dev) return fail_arg("null argument");
+  if (n < 0 || gamma_in < 0 || gamma_in > gamma) return fail_arg("bad llr arguments");
+  if (n && gamma_in) {
+    cudaError_t e = cudaMemcpyAsync(x_dev, x_host, (size_t)n * gamma_in * sizeof(double), cudaMemcpyHostToDevice,
+                                    as_stream(stream));
+    if (e != cudaSuccess) return fail_rt(std::string("llr_from_host: ") + cudaGetErrorString(e));
+  }
+  return qc_llr_from_lane_major(n, gamma, gamma_in, x_dev, sigma, mu_vm, stream);
+}
+
 int qc_llr_from_lane_major(int n, int gamma, int gamma_in, const double* x, double sigma, float* mu_vm,
                            void* stream) {
   if (int r = check_gamma(gamma)) return r;

@@ -74,6 +74,7 @@ def main():
             "push_frame_ms_per_slot": round(dt / a.frames * 1e3, 4),
             "latency_ms_p50": round(lat[len(lat) // 2] * 1e3, 4),
             "latency_ms_p99": round(lat[int(len(lat) * 0.99)] * 1e3, 4),
+            "latency_ms_mean": round(sum(lat) / len(lat) * 1e3, 4), "latency_ms_max": round(lat[-1] * 1e3, 3),
             "frame_latency_ms_p50": round(lat[len(lat) // 2] * 1e3 * window, 2),
             "device_resident_mbit_s": round(dev_rate, 2),
             "device_ms_per_slot": round(dev_ms / pushes, 4),
