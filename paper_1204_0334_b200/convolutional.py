@@ -94,6 +94,12 @@ class StreamDecoder:
 
     Frame t pushed at slot t is emitted at slot t + I*(m_s+1) - 1 after I
     iterations; the first emission happens at slot I*(m_s+1) - 1.
+
+    Emitted frames' arrays live in page-locked host memory (the copy-out is
+    asynchronous); a caller that keeps very many frames alive can switch to
+    ordinary arrays with `set_pinned_outputs(False)` (each push then waits for
+    its copy-out) and return cached page-locked blocks with
+    `release_pinned_cache()`.
     """
 
     def __init__(self, code: LdpcccCode, processors: int, gamma: int = 1):
