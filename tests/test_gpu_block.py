@@ -685,3 +685,30 @@ def test_host_pipeline_compacted_early_stop_equals_plain(gpu):
     assert np.array_equal(r.hard_bits, ref.hard_bits)
     assert np.array_equal(r.posteriors, ref.posteriors)
     assert r.iterations_run.min() < 12 < r.iterations_run.max()
+
+
+def test_decode_outputs_pageable_and_page_locked_agree(gpu):
+    """decode_batch returns page-locked result arrays by default and ordinary
+    ones with set_pinned_outputs(False); small pageable inputs are staged
+    page-locked in one copy, large ones go through the pipeline's staging
+    threads -- identical results on every path."""
+    q = gpu
+    from paper_1204_0334_b200 import bp as qbp
+    h, _ = q.load_code(q.codes.bundled_code_path("n18360"))
+    lay = q.build_edge_layout(h)
+    sigma = q.ebn0_to_sigma(3.0, 5 / 6)
+    y = 1.0 + sigma * np.random.default_rng(3).standard_normal((96, lay.n_vars))
+    ref = q.decode_batch(lay, q.host_array(y), sigma, 20)
+    outs = []
+    for pinned, stage in ((False, qbp.STAGE_PAGEABLE_MAX_BYTES), (True, 0), (False, 0)):
+        q.set_pinned_outputs(pinned)
+        old = qbp.STAGE_PAGEABLE_MAX_BYTES
+        qbp.STAGE_PAGEABLE_MAX_BYTES = stage
+        try:
+            outs.append(q.decode_batch(lay, y, sigma, 20))
+        finally:
+            qbp.STAGE_PAGEABLE_MAX_BYTES = old
+            q.set_pinned_outputs(True)
+    for r in outs:
+        for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
+            assert np.array_equal(getattr(r, f), getattr(ref, f)), f

@@ -206,3 +206,40 @@ def test_lookahead_slots_match_cc_slot(gpu, shape):
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
     assert int(outs[0][3][1].sum()) > 0 or float(np.abs(outs[0][2]).sum()) > 0
+
+
+def test_push_frame_outputs_pageable_and_page_locked_agree(gpu):
+    """Emitted frames land in page-locked arrays (asynchronous copy-out) by
+    default; with set_pinned_outputs(False) they are ordinary numpy arrays and
+    each push waits for its copy.  Same frames, same bits either way; also
+    through push_llr_device and flush."""
+    q = gpu
+    import torch
+    from paper_1204_0334_b200 import bp as qbp
+    code = q.unwrap_qc(q.multiplicative_shifts(4, 24, 11))
+    rng = np.random.default_rng(41)
+    G = 40
+    ys = rng.normal(1.0, 0.8, size=(30, G, code.c))
+    runs = []
+    for pinned in (True, False):
+        q.set_pinned_outputs(pinned)
+        try:
+            dec = q.StreamDecoder(code, 3, gamma=G)
+            out = [f for f in (dec.push_frame(y, 0.8) for y in ys[:20]) if f is not None]
+            gp = (G + 31) // 32 * 32
+            for y in ys[20:]:
+                mu = np.full((code.c, gp), 50.0, dtype=np.float32)
+                mu[:, :G] = np.clip(2.0 * y.T / 0.64, -50, 50)
+                f = dec.push_llr_device(torch.from_numpy(mu).cuda())
+                if f is not None:
+                    out.append(f)
+            out += dec.flush()
+            runs.append(out)
+        finally:
+            q.set_pinned_outputs(True)
+    assert [f.frame_index for f in runs[0]] == [f.frame_index for f in runs[1]]
+    for a, b in zip(*runs):
+        assert np.array_equal(a.posteriors, b.posteriors) and np.array_equal(a.hard_bits, b.hard_bits)
+        assert a.tail == b.tail
+    assert qbp._lib.load().qc_host_is_pinned(runs[0][0].posteriors.ctypes.data, runs[0][0].posteriors.nbytes) == 1
+    assert qbp._lib.load().qc_host_is_pinned(runs[1][0].posteriors.ctypes.data, runs[1][0].posteriors.nbytes) == 0
