@@ -712,3 +712,20 @@ def test_decode_outputs_pageable_and_page_locked_agree(gpu):
     for r in outs:
         for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
             assert np.array_equal(getattr(r, f), getattr(ref, f)), f
+
+
+def test_small_call_chunking_matches_device_decoder(gpu):
+    """decode_batch splits calls from 65 lanes into 64 / 128-lane chunks (bp.py
+    _host_decoder); every size around the break points equals one device
+    BlockDecoder run over the same lanes (toy code, 9 iterations)."""
+    q = gpu
+    lay = toy(q)
+    y = np.random.default_rng(12).normal(1.0, 0.9, size=(255, lay.n_vars))
+    dec = q.BlockDecoder(lay, 256, 9, graph=False, count_bits=False)
+    dec.load_lane_major(y, 0.9)
+    dec.run()
+    ref = dec.result(255)
+    for G in (1, 33, 64, 65, 96, 127, 128, 129, 200, 255):
+        r = q.decode_batch(lay, y[:G], 0.9, 9)
+        for f in ("hard_bits", "posteriors", "syndrome_ok", "iterations_run"):
+            assert np.array_equal(getattr(r, f), getattr(ref, f)[:G]), (G, f)
