@@ -580,21 +580,34 @@ __device__ __forceinline__ unsigned div_magic(unsigned x, unsigned long long m) 
 }
 
 // parity of check m over its d_c variables' hard bits, 32 lanes per word
+// AGG_SYN_K consecutive checks per thread, their failures OR-ed into one
+// atomic (K-fold fewer syndrome CTAs and atomics per launch)
+#ifndef AGG_SYN_K
+#define AGG_SYN_K 8   // 1 -> 8: early-stop decode -0.7-1.4% (3.2 / 3.6 dB, gamma 4096)
+#endif
+__host__ __device__ __forceinline__ int es_syn_rows(int M) { return (M + AGG_SYN_K - 1) / AGG_SYN_K; }
+
 template <int DC>
 __device__ __forceinline__ void es_syndrome_block(const EsFused& e, const QcGrid& grid, unsigned blk, int M) {
   const long long idx = (long long)blk * AGG_THREADS + threadIdx.x;
-  if (idx >= (long long)M * e.s_W) return;
-  const int m = (int)(idx / e.s_W), w = e.s_w0 + (int)(idx - (long long)m * e.s_W);
+  if (idx >= (long long)es_syn_rows(M) * e.s_W) return;
+  const int mb = (int)(idx / e.s_W), w = e.s_w0 + (int)(idx - (long long)mb * e.s_W);
   if (e.s_act && e.s_act[w] == 0u) return;
-  const int j = div_p(grid, m), r = m - j * grid.p;
-  uint32_t par = 0;
+  uint32_t acc = 0;
+  const int m0 = mb * AGG_SYN_K, m1 = min(M, m0 + AGG_SYN_K);
+#pragma unroll 2
+  for (int m = m0; m < m1; ++m) {
+    const int j = div_p(grid, m), r = m - j * grid.p;
+    uint32_t par = 0;
 #pragma unroll
-  for (int k = 0; k < DC; ++k) {
-    int c = r + grid.s[j * grid.L + k];
-    c -= (c >= grid.p) ? grid.p : 0;
-    par ^= e.hb[(size_t)(k * grid.p + c) * e.Wt + w];
+    for (int k = 0; k < DC; ++k) {
+      int c = r + grid.s[j * grid.L + k];
+      c -= (c >= grid.p) ? grid.p : 0;
+      par ^= e.hb[(size_t)(k * grid.p + c) * e.Wt + w];
+    }
+    acc |= par;
   }
-  if (par) atomicOr(e.s_bad + w, par);
+  if (acc) atomicOr(e.s_bad + w, acc);
 }
 
 __device__ __forceinline__ void es_update_block(const EsFused& e) {
@@ -917,7 +930,7 @@ int launch_agg_fused_es(const qc_plan* p, int gamma, int lanes, int v0, int flag
   unsigned extra = 0;
   if (es) {
     f.es = *es;
-    f.es.nbs = es->s_W > 0 ? (int)(((long long)p->M * es->s_W + AGG_THREADS - 1) / AGG_THREADS) : 0;
+    f.es.nbs = es->s_W > 0 ? (int)(((long long)es_syn_rows(p->M) * es->s_W + AGG_THREADS - 1) / AGG_THREADS) : 0;
     const unsigned jobs = (unsigned)f.es.nbs + (es->u_W > 0 ? 1u : 0u);
     extra = (jobs + f.R) / (f.R + 1);
   }
